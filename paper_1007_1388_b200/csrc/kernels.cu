@@ -1,0 +1,471 @@
+// kernels.cu -- sm_100a kernels of the D3Q19 LBGK patch solver.
+//
+// The hot loop is sweep_kernel: the fused pull stream + bounce-back + BGK
+// collide update of eq:lbm / eq:feq with centred PDFs,
+// pull streaming from two grids and half-way bounce-back with a
+// moving-wall term.  SoA layout: one q-slice per
+// direction, rows padded so interior x = 0 is aligned.  The
+// kernel is HBM-bound: 19 loads + 19 stores of sizeof(real) per fluid cell
+// (P:1075-1082), no data reuse across directions (each src element is pulled
+// by exactly one cell), so there is nothing to stage in shared memory; the
+// design goal is enough independent loads in flight per SM and fully
+// coalesced, sector-aligned stores.
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lbm {
+
+__device__ __forceinline__ int64_t cell_index(const Geom &g, int x, int y, int z)
+{
+    return ((int64_t)(z + 1) * g.py + (y + 1)) * (int64_t)g.px + (x + g.xo);
+}
+
+template <typename real>
+__device__ __forceinline__ real ld_stream(const real *p)
+{
+    return __ldg(p);
+}
+
+template <typename real>
+__device__ __forceinline__ void st_stream(real *p, real v)
+{
+    __stcs(p, v);  // evict-first: dst is not re-read in this sweep
+}
+
+// BGK collision of the pulled values (eq:lbm with eq:feq, centred, rho0 = 1):
+//   drho = sum p_i, u = sum e_i p_i / rho0,
+//   p_i <- p_i - omega (p_i - w_i [drho + 3 e_i.u + 4.5 (e_i.u)^2 - 1.5 u.u])
+// evaluated pairwise for opposite directions (e.u changes sign, the even part
+// of f^eq is shared).
+template <typename real>
+__device__ __forceinline__ void collide(real (&p)[Q], real omega)
+{
+    const real drho = p[0] + p[1] + p[2] + p[3] + p[4] + p[5] + p[6] + p[7] + p[8] + p[9] + p[10] + p[11] +
+                      p[12] + p[13] + p[14] + p[15] + p[16] + p[17] + p[18];
+    const real ux = (p[1] - p[2]) + (p[7] - p[8]) + (p[9] - p[10]) + (p[11] - p[12]) + (p[13] - p[14]);
+    const real uy = (p[3] - p[4]) + (p[7] - p[8]) - (p[9] - p[10]) + (p[15] - p[16]) + (p[17] - p[18]);
+    const real uz = (p[5] - p[6]) + (p[11] - p[12]) - (p[13] - p[14]) + (p[15] - p[16]) - (p[17] - p[18]);
+    const real c0 = real(1) - omega;
+    const real base = drho - real(1.5) * (ux * ux + uy * uy + uz * uz);
+    const real w0 = omega * real(1.0 / 3.0);
+    const real w1 = omega * real(1.0 / 18.0);
+    const real w2 = omega * real(1.0 / 36.0);
+    p[0] = c0 * p[0] + w0 * base;
+#define LBM_PAIR(a, b, eu, w)                              \
+    {                                                      \
+        const real e_ = (eu);                              \
+        const real t_ = base + real(4.5) * e_ * e_;        \
+        const real s_ = real(3) * e_;                      \
+        p[a] = c0 * p[a] + (w) * (t_ + s_);                \
+        p[b] = c0 * p[b] + (w) * (t_ - s_);                \
+    }
+    LBM_PAIR(1, 2, ux, w1)
+    LBM_PAIR(3, 4, uy, w1)
+    LBM_PAIR(5, 6, uz, w1)
+    LBM_PAIR(7, 8, ux + uy, w2)
+    LBM_PAIR(9, 10, ux - uy, w2)
+    LBM_PAIR(11, 12, ux + uz, w2)
+    LBM_PAIR(13, 14, ux - uz, w2)
+    LBM_PAIR(15, 16, uy + uz, w2)
+    LBM_PAIR(17, 18, uy - uz, w2)
+#undef LBM_PAIR
+}
+
+template <typename real>
+__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY) sweep_kernel(const SweepArgs<real> a)
+{
+    // Locate this block's box (binary search over the tile prefix sums).
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int64_t t = b - a.tile_prefix[lo];
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = (int)(t % tiles_x);
+    t /= tiles_x;
+    const int ty = (int)(t % tiles_y);
+    const int tz = (int)(t / tiles_y);
+    const int x = bx.lo[0] + tx * SWEEP_BX + (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    if (x >= bx.lo[0] + bx.n[0] || y >= bx.lo[1] + bx.n[1]) return;
+
+    const Geom &g = a.g;
+    const int64_t cell = cell_index(g, x, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k = a.kind[fbase];
+    if (k == 2) return;  // non-fluid: never updated (R13)
+
+    const real *s = a.src + pbase;
+    const int64_t qs = g.qs;
+    real p[Q];
+    // Pull with flag-driven half-way bounce-back (R3):
+    //   neighbour x - e_i fluid  -> p_i = src_i(x - e_i)
+    //   no-slip wall             -> p_i = src_opp(i)(x)
+    //   moving wall k            -> p_i = src_opp(i)(x) + 6 w_i rho0 e_i.u_w[k]
+    uint8_t nb[Q];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+        const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+        nb[i] = k ? a.flags[fbase - sh] : (uint8_t)0;
+    }
+    p[0] = ld_stream(s);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+        const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+        const real *addr = nb[i] ? s + OPP(i) * qs : s + i * qs - sh;
+        p[i] = ld_stream(addr);
+    }
+    if (k) {
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+            if (nb[i] >= 2) p[i] += a.corr[(nb[i] - 2) * Q + i];
+    }
+    collide<real>(p, a.omega);
+    real *d = a.dst + pbase;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) st_stream(d + i * qs, p[i]);
+}
+
+template <typename real>
+cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, cudaStream_t s)
+{
+    if (total_tiles <= 0) return cudaSuccess;
+    dim3 block(SWEEP_BX, SWEEP_BY, 1);
+    sweep_kernel<real><<<(unsigned)total_tiles, block, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- ghost exchange copies
+template <typename real>
+__global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs, const real *grid_src,
+                                                            real *grid_dst, const real *buf_src,
+                                                            real *buf_dst, const Geom g)
+{
+    const CopySeg &sg = segs[blockIdx.y];
+    const int64_t nelem = sg.nelem, cells = sg.cells;
+    const int s0 = sg.size[0], s1 = sg.size[1];
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nelem;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int qi = (int)(e / cells);
+        const int64_t c = e - (int64_t)qi * cells;
+        const int cx = (int)(c % s0);
+        const int64_t r = c / s0;
+        const int cy = (int)(r % s1);
+        const int cz = (int)(r / s1);
+        const int q = sg.q[qi];
+        real v;
+        if (sg.src_is_buf)
+            v = buf_src[sg.src_base + e];
+        else
+            v = grid_src[sg.src_base + q * g.qs +
+                         cell_index(g, sg.src_lo[0] + cx, sg.src_lo[1] + cy, sg.src_lo[2] + cz)];
+        if (sg.dst_is_buf)
+            buf_dst[sg.dst_base + e] = v;
+        else
+            grid_dst[sg.dst_base + q * g.qs +
+                     cell_index(g, sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz)] = v;
+    }
+}
+
+template <typename real>
+cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
+                                 real *grid_dst, const real *buf_src, real *buf_dst, const Geom &g,
+                                 cudaStream_t s)
+{
+    if (nseg <= 0 || max_elems <= 0) return cudaSuccess;
+    int64_t bx = (max_elems + 255) / 256;
+    if (bx > 1024) bx = 1024;
+    for (int off = 0; off < nseg; off += 65535) {
+        int n = nseg - off < 65535 ? nseg - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n, 1);
+        copy_segments_kernel<real><<<grid, 256, 0, s>>>(segs + off, grid_src, grid_dst, buf_src, buf_dst, g);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- flags
+__global__ void build_flags_kernel(const uint8_t *global, int64_t nx, int64_t ny, int64_t nz, int p0, int p1,
+                                   int p2, const int *origin, const Geom g, uint8_t *flags)
+{
+    const int lp = blockIdx.y;
+    const int64_t total = g.fs;
+    const int periodic[3] = {p0, p1, p2};
+    const int64_t n[3] = {nx, ny, nz};
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int col = (int)(e % g.px);
+        const int64_t r = e / g.px;
+        const int row = (int)(r % g.py);
+        const int pl = (int)(r / g.py);
+        const int lc[3] = {col - g.xo, row - 1, pl - 1};
+        uint8_t v = 1;
+        if (lc[0] >= -1 && lc[0] <= g.n[0]) {
+            int64_t c[3];
+            bool ok = true;
+            for (int ax = 0; ax < 3; ++ax) {
+                c[ax] = origin[3 * lp + ax] + lc[ax];
+                if (periodic[ax]) c[ax] = (c[ax] + n[ax]) % n[ax];
+                if (c[ax] < -1 || c[ax] > n[ax]) ok = false;
+            }
+            if (ok) v = global[((c[2] + 1) * (ny + 2) + (c[1] + 1)) * (nx + 2) + (c[0] + 1)];
+        }
+        flags[(int64_t)lp * g.fs + e] = v;
+    }
+}
+
+// kind: 2 = non-fluid (or ghost / padding), 1 = fluid with a non-fluid
+// neighbour among the 18 (needs the flag-driven path), 0 = fluid with only
+// fluid neighbours (pure pull).
+__global__ void build_kind_kernel(const Geom g, const uint8_t *flags, uint8_t *kind)
+{
+    const int lp = blockIdx.y;
+    const int64_t total = g.fs;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int col = (int)(e % g.px);
+        const int64_t r = e / g.px;
+        const int row = (int)(r % g.py);
+        const int pl = (int)(r / g.py);
+        const int x = col - g.xo, y = row - 1, z = pl - 1;
+        const uint8_t *f = flags + (int64_t)lp * g.fs;
+        uint8_t kd = 2;
+        if (x >= 0 && x < g.n[0] && y >= 0 && y < g.n[1] && z >= 0 && z < g.n[2] && f[e] == 0) {
+            kd = 0;
+            for (int i = 1; i < Q; ++i) {
+                const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+                if (f[e - sh] != 0) kd = 1;
+            }
+        }
+        kind[(int64_t)lp * g.fs + e] = kd;
+    }
+}
+
+cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], const int periodic[3],
+                               const int *patch_origin, int nlocal, const Geom &g, uint8_t *flags,
+                               uint8_t *kind, cudaStream_t s)
+{
+    int64_t bx = (g.fs + 255) / 256;
+    if (bx > 4096) bx = 4096;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n);
+        build_flags_kernel<<<grid, 256, 0, s>>>(global, domain[0], domain[1], domain[2], periodic[0], periodic[1],
+                                                periodic[2], patch_origin + 3 * off, g, flags + (int64_t)off * g.fs);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n);
+        build_kind_kernel<<<grid, 256, 0, s>>>(g, flags + (int64_t)off * g.fs, kind + (int64_t)off * g.fs);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- import / export
+struct OwnedMap {
+    int64_t lo[3];
+    int64_t n[3];
+    int brick[3];
+};
+
+__device__ __forceinline__ void owned_to_patch(const Geom &g, const int brick[3], int64_t ox, int64_t oy,
+                                               int64_t oz, int &lp, int &lx, int &ly, int &lz)
+{
+    const int bx = (int)(ox / g.n[0]), by = (int)(oy / g.n[1]), bz = (int)(oz / g.n[2]);
+    lx = (int)(ox - (int64_t)bx * g.n[0]);
+    ly = (int)(oy - (int64_t)by * g.n[1]);
+    lz = (int)(oz - (int64_t)bz * g.n[2]);
+    lp = (bz * brick[1] + by) * brick[0] + bx;
+}
+
+template <typename real>
+__global__ void import_kernel(const double *canon, int64_t z0, int64_t ncells, int64_t nx, int64_t ny,
+                              int b0, int b1, int b2, const Geom g, real *grid)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = z0 + r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) gp[q * g.qs] = (real)canon[c * Q + q];
+    }
+}
+
+template <typename real>
+__global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0, int64_t ncells, int64_t nx,
+                              int64_t ny, int b0, int b1, int b2, const Geom g, int mode, double *canon,
+                              double *rho, double *u)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = z0 + r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        const int64_t ci = cell_index(g, lx, ly, lz);
+        const bool fluid = flags[(int64_t)lp * g.fs + ci] == 0;
+        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        if (mode == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? (double)gp[q * g.qs] : 0.0;
+        } else {
+            // Macroscopic export: rho = rho0 + sum f~, u = sum e f~ / rho0.
+            double s = 0, jx = 0, jy = 0, jz = 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const double v = (double)gp[q * g.qs];
+                s += v;
+                jx += EX(q) * v;
+                jy += EY(q) * v;
+                jz += EZ(q) * v;
+            }
+            if (rho) rho[c] = fluid ? 1.0 + s : 0.0;
+            if (u) {
+                u[3 * c] = fluid ? jx : 0.0;
+                u[3 * c + 1] = fluid ? jy : 0.0;
+                u[3 * c + 2] = fluid ? jz : 0.0;
+            }
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, const int64_t owned_lo[3],
+                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid,
+                          cudaStream_t s)
+{
+    (void)owned_lo;
+    const int64_t ncells = owned_n[0] * owned_n[1] * nz_chunk;
+    if (ncells <= 0) return cudaSuccess;
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 8192) nb = 8192;
+    import_kernel<real><<<(unsigned)nb, 256, 0, s>>>(canon, z0, ncells, owned_n[0], owned_n[1], brick[0],
+                                                    brick[1], brick[2], g, grid);
+    return cudaGetLastError();
+}
+
+template <typename real>
+cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, int64_t nz_chunk,
+                          const int64_t owned_lo[3], const int64_t owned_n[3], const int brick[3],
+                          const Geom &g, double *canon, int mode, double *rho, double *u, cudaStream_t s)
+{
+    (void)owned_lo;
+    const int64_t ncells = owned_n[0] * owned_n[1] * nz_chunk;
+    if (ncells <= 0) return cudaSuccess;
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 8192) nb = 8192;
+    export_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, flags, z0, ncells, owned_n[0], owned_n[1], brick[0],
+                                                    brick[1], brick[2], g, mode, canon, rho, u);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- seeded noise (input generator)
+// Same counter-based generator as paper_1007_1388_b200/inputs.py (not part of
+// the method): k = splitmix64(global_index * 19 + q + seed * golden) % 2049 - 1024.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename real>
+__global__ void noise_kernel(real *grid, uint64_t seed, int64_t NX, int64_t NY, int64_t lox, int64_t loy,
+                             int64_t loz, int64_t nx, int64_t ny, int64_t ncells, int b0, int b1, int b2,
+                             const Geom g)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        const uint64_t gi = (uint64_t)(((loz + oz) * NY + (loy + oy)) * NX + (lox + ox));
+        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t key = gi * 19ull + (uint64_t)q + seed * 0x9E3779B97F4A7C15ull;
+            const int64_t k = (int64_t)(splitmix64(key) % 2049ull) - 1024;
+            gp[q * g.qs] = (real)((double)k * (1.0 / 1048576.0));
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_noise(real *grid, uint64_t seed, const int64_t domain[3], const int64_t owned_lo[3],
+                         const int64_t owned_n[3], const int brick[3], const Geom &g, cudaStream_t s)
+{
+    const int64_t ncells = owned_n[0] * owned_n[1] * owned_n[2];
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 16384) nb = 16384;
+    noise_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, seed, domain[0], domain[1], owned_lo[0], owned_lo[1],
+                                                   owned_lo[2], owned_n[0], owned_n[1], ncells, brick[0], brick[1],
+                                                   brick[2], g);
+    return cudaGetLastError();
+}
+
+template <typename real>
+__global__ void gather_kernel(const real *grid, const uint8_t *flags, const int64_t *xyz, int64_t n, int b0,
+                              int b1, int b2, const Geom g, double *out)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, xyz[3 * c], xyz[3 * c + 1], xyz[3 * c + 2], lp, lx, ly, lz);
+        const int64_t ci = cell_index(g, lx, ly, lz);
+        const bool fluid = flags[(int64_t)lp * g.fs + ci] == 0;
+        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? (double)gp[q * g.qs] : 0.0;
+    }
+}
+
+template <typename real>
+cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t *xyz_local, int64_t n,
+                          const int brick[3], const Geom &g, double *out, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    int64_t nb = (n + 127) / 128;
+    if (nb > 4096) nb = 4096;
+    gather_kernel<real><<<(unsigned)nb, 128, 0, s>>>(grid, flags, xyz_local, n, brick[0], brick[1], brick[2], g, out);
+    return cudaGetLastError();
+}
+
+#define LBM_INSTANTIATE(real)                                                                                   \
+    template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, cudaStream_t);                    \
+    template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
+                                                    const real *, real *, const Geom &, cudaStream_t);          \
+    template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
+                                             const int *, const Geom &, real *, cudaStream_t);                 \
+    template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \
+                                             const int64_t *, const int *, const Geom &, double *, int,        \
+                                             double *, double *, cudaStream_t);                                \
+    template cudaError_t launch_noise<real>(real *, uint64_t, const int64_t *, const int64_t *, const int64_t *, \
+                                            const int *, const Geom &, cudaStream_t);                          \
+    template cudaError_t launch_gather<real>(const real *, const uint8_t *, const int64_t *, int64_t,            \
+                                             const int *, const Geom &, double *, cudaStream_t);
+
+LBM_INSTANTIATE(float)
+LBM_INSTANTIATE(double)
+
+}  // namespace lbm

@@ -1,0 +1,61 @@
+// kernels.cuh -- launch wrappers of the sm_100a kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lbm_internal.h"
+
+namespace lbm {
+
+// Sweep launch configuration: BX threads along x (one warp-row = 32 cells),
+// BY rows along y per block.
+constexpr int SWEEP_BX = 64;
+constexpr int SWEEP_BY = 4;
+
+template <typename real>
+struct SweepArgs {
+    const real *src;
+    real *dst;
+    const uint8_t *flags;   // [patch][fs] raw cell flags incl. ghost layer
+    const uint8_t *kind;    // [patch][fs] 0 fluid (all neighbours fluid), 1 fluid next to a wall, 2 non-fluid
+    const real *corr;       // [nvel][19]: 6 w_i rho0 (e_i . u_w[k]) rounded to real
+    Geom g;
+    real omega;
+    const Box *boxes;       // device
+    const int64_t *tile_prefix; // device, nboxes + 1
+    int nboxes;
+};
+
+template <typename real>
+cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, cudaStream_t s);
+
+template <typename real>
+cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
+                                 real *grid_dst, const real *buf_src, real *buf_dst, const Geom &g,
+                                 cudaStream_t s);
+
+// Build per-patch flags (incl. ghosts, periodic wrap) from the global flag
+// array (device copy, (nz+2)(ny+2)(nx+2)), then the per-cell kind.
+cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], const int periodic[3],
+                               const int *patch_origin /*3 per local patch*/, int nlocal, const Geom &g,
+                               uint8_t *flags, uint8_t *kind, cudaStream_t s);
+
+// Import / export between the canonical double [z][y][x][19] layout of a
+// range of owned z-planes and the patch grids.
+template <typename real>
+cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, const int64_t owned_lo[3],
+                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid,
+                          cudaStream_t s);
+template <typename real>
+cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, int64_t nz_chunk,
+                          const int64_t owned_lo[3], const int64_t owned_n[3], const int brick[3],
+                          const Geom &g, double *canon, int mode /*0 pdfs, 1 macroscopic*/, double *rho,
+                          double *u, cudaStream_t s);
+template <typename real>
+cudaError_t launch_noise(real *grid, uint64_t seed, const int64_t domain[3], const int64_t owned_lo[3],
+                         const int64_t owned_n[3], const int brick[3], const Geom &g, cudaStream_t s);
+template <typename real>
+cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t *xyz_local /*3 per cell*/,
+                          int64_t n, const int brick[3], const Geom &g, double *out, cudaStream_t s);
+
+}  // namespace lbm

@@ -1,0 +1,126 @@
+// lbm_internal.h -- internal definitions of the B200 D3Q19 patch solver.
+// Product code: shares nothing with oracle/ (own direction table, own layouts).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "lbm.h"
+
+namespace lbm {
+
+constexpr int Q = 19;
+
+// Frozen D3Q19 order (include/lbm.h, R2).  Opposites are i, i+1.
+// P:403-405 (D3Q19), P:441-442 (weights 1/3, 1/18, 1/36).  Stored as bit
+// masks so that host and device code fold them at compile time.
+//   i : 0 | 1 2 3 4 5 6 | 7 8 9 10 11 12 13 14 15 16 17 18
+constexpr unsigned kXP = (1u << 1) | (1u << 7) | (1u << 9) | (1u << 11) | (1u << 13);
+constexpr unsigned kXM = (1u << 2) | (1u << 8) | (1u << 10) | (1u << 12) | (1u << 14);
+constexpr unsigned kYP = (1u << 3) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 17);
+constexpr unsigned kYM = (1u << 4) | (1u << 8) | (1u << 9) | (1u << 16) | (1u << 18);
+constexpr unsigned kZP = (1u << 5) | (1u << 11) | (1u << 14) | (1u << 15) | (1u << 18);
+constexpr unsigned kZM = (1u << 6) | (1u << 12) | (1u << 13) | (1u << 16) | (1u << 17);
+__host__ __device__ constexpr int EXf(int i) { return (int)((kXP >> i) & 1u) - (int)((kXM >> i) & 1u); }
+__host__ __device__ constexpr int EYf(int i) { return (int)((kYP >> i) & 1u) - (int)((kYM >> i) & 1u); }
+__host__ __device__ constexpr int EZf(int i) { return (int)((kZP >> i) & 1u) - (int)((kZM >> i) & 1u); }
+__host__ __device__ constexpr int OPPf(int i) { return i == 0 ? 0 : ((i & 1) ? i + 1 : i - 1); }
+__host__ __device__ constexpr double Wf(int i) { return i == 0 ? 1.0 / 3.0 : (i <= 6 ? 1.0 / 18.0 : 1.0 / 36.0); }
+#define EX(i) ::lbm::EXf(i)
+#define EY(i) ::lbm::EYf(i)
+#define EZ(i) ::lbm::EZf(i)
+#define OPP(i) ::lbm::OPPf(i)
+#define WQ(i) ::lbm::Wf(i)
+
+// The 18 patch-neighbour directions (6 faces + 12 edges; D3Q19 has no corner
+// velocities, so corner ghosts are never read).  Fixed order = ABI of the
+// exchange plan: lexicographic over (dz, dy, dx) in {-1,0,1}^3 minus the
+// centre and the 8 corners.
+constexpr int NDIR = 18;
+struct Dir3 { int d[3]; };
+
+// Patch geometry shared by every patch of a ctx (all patches have one size).
+// Element index of cell (x, y, z), -1 <= x,y,z <= n, inside one q-slice:
+//   ((z + 1) * py + (y + 1)) * px + (x + xo)
+// px is padded so that x = 0 starts on an `align`-byte boundary; q-slices and
+// patches are laid out back to back: [patch][q][z][y][x].
+struct Geom {
+    int n[3];        // patch interior size
+    int px, py;      // row pitch (elements), rows per plane (n[1] + 2)
+    int xo;          // element offset of interior x = 0 in a row
+    int64_t plane;   // px * py
+    int64_t qs;      // elements per q-slice = plane * (n[2] + 2)
+    int64_t ps;      // elements per patch = 19 * qs
+    int64_t fs;      // flag bytes per patch = qs
+};
+
+// Sweep box: cells [lo, lo + n) of local patch `patch`.
+struct Box {
+    int patch;
+    int lo[3];
+    int n[3];
+    int tiles_x, tiles_y;
+};
+
+// Copy segment of the ghost exchange (pack, local copy or unpack).
+// src/dst are either a PDF grid region (cells lo..lo+size of local patch at
+// element base) or a linear buffer at element base.  Element order inside a
+// segment: q-list major, then cells x fastest.
+struct CopySeg {
+    int64_t src_base, dst_base;
+    int32_t src_is_buf, dst_is_buf;
+    int32_t src_lo[3], dst_lo[3], size[3];
+    int32_t nq;
+    int32_t q[5];
+    int64_t cells;
+    int64_t nelem;
+};
+
+// Host-only decomposition (no CUDA): plan.cpp.
+struct Seg {
+    int recv_patch, send_patch;   // global patch ids
+    int dir;                      // direction index (0..17) from receiver to sender
+    int d[3];
+    int nq, q[5];
+    int size[3];
+    int recv_lo[3];               // ghost region in the receiving patch (local coords)
+    int send_lo[3];               // boundary region in the sending patch
+    int64_t cells;
+    int peer;                     // other rank (remote) or own rank
+    int64_t offset;               // element offset inside the peer message
+};
+
+struct Decomp {
+    int64_t domain[3];
+    int patch[3];
+    int pgrid[3];        // patches per axis (global)
+    int proc[3];         // ranks per axis
+    int coord[3];        // this rank's coordinate
+    int brick[3];        // patches per rank per axis
+    int rank, nranks;
+    int periodic[3];
+    int force_buffers;
+    int64_t owned_lo[3], owned_hi[3];
+    int nlocal;                   // local patches
+    // local patch l <-> global id; local order = brick-local z, y, x
+    int local_to_global(int l) const;
+    int global_to_local(int g) const;   // -1 if not owned
+    int owner(int g) const;
+    void patch_coord(int g, int c[3]) const;
+    int patch_id(const int c[3]) const;
+};
+
+// Returns an error message (empty on success).
+const char *decompose(const lbm_config &cfg, Decomp &dec);
+// Build the segment lists: local copies, sends and receives (sorted per peer
+// in the canonical (receiving patch, dir) order, offsets filled in).
+struct SegLists {
+    std::vector<Seg> local;   // same-rank ghost copies (exchange_mode AUTO)
+    std::vector<Seg> send;    // grouped by peer (ascending), canonical order inside
+    std::vector<Seg> recv;
+};
+void build_segments(const Decomp &dec, SegLists &out);
+extern const Dir3 kDirs[NDIR];
+
+}  // namespace lbm

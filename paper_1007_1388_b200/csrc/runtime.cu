@@ -1,0 +1,1258 @@
+// runtime.cu -- patch runtime and C ABI (include/lbm.h) of the B200 solver.
+//
+// One process per GPU; each rank owns a brick of patches (the paper's
+// Blocks) stored back to back in one SoA allocation per PDF grid
+// (two grids).  A time step (the paper's Sweep) is:
+//   sweep (fused pull + BB + collide, kernels.cu)  ->  ghost exchange
+//   (extract = pack / local copy, transport = NCCL send/recv, insert = unpack;
+//   P:287-313).  With overlap on, the patch shells facing remote
+//   neighbours are swept first, packed and sent on a second stream while the
+//   interiors are swept (the paper sums these times).  Steps are
+//   captured pairwise (src/dst swap) in a CUDA graph and replayed.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lbm_internal.h"
+
+using namespace lbm;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+constexpr int kAlignDefault = 128;  // bytes; interior x = 0 of every row starts on this boundary
+constexpr int kTimingSlots = 64;
+enum Phase { PH_SWEEP = 0, PH_SHELL = 1, PH_INTERIOR = 2, PH_PACK = 3, PH_NCCL = 4, PH_UNPACK = 5, PH_STEP = 6 };
+constexpr int kEvPerSlot = 14;
+
+struct DevBoxes {
+    Box *boxes = nullptr;
+    int64_t *prefix = nullptr;
+    int n = 0;
+    int64_t tiles = 0;
+};
+
+struct DevSegs {
+    CopySeg *segs = nullptr;
+    int n = 0;
+    int64_t max_elems = 0;
+    int64_t total_elems = 0;
+};
+
+struct Peer {
+    int rank;
+    int64_t send_off, send_n, recv_off, recv_n;
+};
+
+struct TimingSlot {
+    cudaEvent_t ev[kEvPerSlot];
+    bool used = false;
+    bool overlap = false;
+};
+
+}  // namespace
+
+struct lbm_ctx {
+    lbm_config cfg;
+    Decomp dec;
+    Geom g;
+    int esize = 8;
+    int device = 0;
+    int align = kAlignDefault;
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    bool own_stream = false;
+    void *grid[2] = {nullptr, nullptr};
+    int cur = 0;
+    uint8_t *flags = nullptr, *kind = nullptr;
+    void *corr = nullptr;
+    int *d_origin = nullptr;
+    SegLists segs;
+    DevSegs pack_all;   // pack + local copies (non-overlapped step / ghost refresh)
+    DevSegs pack_remote, local_copy, unpack;
+    void *sendbuf = nullptr, *recvbuf = nullptr;
+    int64_t send_elems = 0, recv_elems = 0;
+    std::vector<Peer> peers;
+    bool has_remote = false;   // anything goes through buffers
+    bool has_nccl = false;     // a peer other than this rank
+    ncclComm_t nccl = nullptr;
+    DevBoxes box_all, box_shell, box_interior;
+    bool use_overlap = false;
+    int64_t fluid_local = 0, fluid_global = 0;
+    bool flags_set = false;
+    int64_t steps = 0, launches = 0;
+    int64_t launches_per_step = 0;
+    int64_t device_bytes = 0;
+    std::string err;
+    bool poisoned = false;
+    bool timing = false;
+    double phase_ms[LBM_NPHASES] = {0};
+    int64_t phase_count[LBM_NPHASES] = {0};
+    TimingSlot slots[kTimingSlots];
+    int slot_next = 0;
+    bool events_created = false;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    int64_t graph_launches[2] = {0, 0};
+
+    lbm_status fail(lbm_status st, const std::string &m)
+    {
+        err = m;
+        if (st == LBM_ERR_CUDA || st == LBM_ERR_NCCL || st == LBM_ERR_INTERNAL) poisoned = true;
+        return st;
+    }
+    lbm_status cuda_fail(cudaError_t e, const char *what, int line)
+    {
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s [runtime.cu:%d]", cudaGetErrorName(e),
+                      cudaGetErrorString(e), what, line);
+        if (e == cudaErrorMemoryAllocation) {
+            err = buf;
+            return LBM_ERR_OOM;
+        }
+        return fail(LBM_ERR_CUDA, buf);
+    }
+    lbm_status nccl_fail(ncclResult_t r, const char *what, int line)
+    {
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "NCCL error %d (%s) in %s [runtime.cu:%d]", (int)r, ncclGetErrorString(r), what,
+                      line);
+        return fail(LBM_ERR_NCCL, buf);
+    }
+};
+
+#define CK(call)                                                              \
+    do {                                                                      \
+        cudaError_t e_ = (call);                                              \
+        if (e_ != cudaSuccess) return ctx->cuda_fail(e_, #call, __LINE__);    \
+    } while (0)
+#define NK(call)                                                              \
+    do {                                                                      \
+        ncclResult_t r_ = (call);                                             \
+        if (r_ != ncclSuccess) return ctx->nccl_fail(r_, #call, __LINE__);    \
+    } while (0)
+#define CHECK_CTX(ctx)                                                        \
+    do {                                                                      \
+        if (!(ctx)) return LBM_ERR_ARG;                                       \
+        if ((ctx)->poisoned) return LBM_ERR_STATE;                            \
+        cudaError_t e_ = cudaSetDevice((ctx)->device);                        \
+        if (e_ != cudaSuccess) return (ctx)->cuda_fail(e_, "cudaSetDevice", __LINE__); \
+    } while (0)
+
+namespace {
+
+template <typename T>
+lbm_status dev_alloc(lbm_ctx *ctx, T **p, size_t bytes)
+{
+    *p = nullptr;
+    if (bytes == 0) return LBM_OK;
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+        ctx->err = buf;
+        return e == cudaErrorMemoryAllocation ? LBM_ERR_OOM : ctx->fail(LBM_ERR_CUDA, buf);
+    }
+    ctx->device_bytes += (int64_t)bytes;
+    return LBM_OK;
+}
+
+Geom make_geom(const int n[3], int esize, int align)
+{
+    Geom g;
+    for (int a = 0; a < 3; ++a) g.n[a] = n[a];
+    const int ae = align / esize;             // elements per alignment unit
+    g.xo = ae;                                // x = -1 sits right before the aligned x = 0
+    g.px = ((g.xo + n[0] + 1 + ae - 1) / ae) * ae;
+    g.py = n[1] + 2;
+    g.plane = (int64_t)g.px * g.py;
+    g.qs = g.plane * (n[2] + 2);
+    g.ps = (int64_t)Q * g.qs;
+    g.fs = g.qs;
+    return g;
+}
+
+Box make_box(int patch, const int lo[3], const int n[3])
+{
+    Box b;
+    b.patch = patch;
+    for (int a = 0; a < 3; ++a) {
+        b.lo[a] = lo[a];
+        b.n[a] = n[a];
+    }
+    b.tiles_x = (n[0] + SWEEP_BX - 1) / SWEEP_BX;
+    b.tiles_y = (n[1] + SWEEP_BY - 1) / SWEEP_BY;
+    return b;
+}
+
+lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &out)
+{
+    std::vector<int64_t> prefix(boxes.size() + 1, 0);
+    for (size_t i = 0; i < boxes.size(); ++i) {
+        const Box &b = boxes[i];
+        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0) ? (int64_t)b.tiles_x * b.tiles_y * b.n[2] : 0;
+        prefix[i + 1] = prefix[i] + t;
+    }
+    out.n = (int)boxes.size();
+    out.tiles = prefix.back();
+    if (boxes.empty()) return LBM_OK;
+    lbm_status st = dev_alloc(ctx, &out.boxes, boxes.size() * sizeof(Box));
+    if (st) return st;
+    st = dev_alloc(ctx, &out.prefix, prefix.size() * sizeof(int64_t));
+    if (st) return st;
+    CK(cudaMemcpy(out.boxes, boxes.data(), boxes.size() * sizeof(Box), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(out.prefix, prefix.data(), prefix.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    return LBM_OK;
+}
+
+lbm_status upload_segs(lbm_ctx *ctx, const std::vector<CopySeg> &v, DevSegs &out)
+{
+    out.n = (int)v.size();
+    out.max_elems = 0;
+    out.total_elems = 0;
+    for (const CopySeg &s : v) {
+        out.max_elems = std::max(out.max_elems, s.nelem);
+        out.total_elems += s.nelem;
+    }
+    if (v.empty()) return LBM_OK;
+    lbm_status st = dev_alloc(ctx, &out.segs, v.size() * sizeof(CopySeg));
+    if (st) return st;
+    CK(cudaMemcpy(out.segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+    return LBM_OK;
+}
+
+CopySeg grid_to_x(const lbm_ctx *ctx, const Seg &s, bool to_buffer, int64_t buf_base)
+{
+    // Source: the sender's boundary layer (a local patch); destination: either
+    // the receiver's ghost layer (local copy) or the send buffer.
+    CopySeg c;
+    std::memset(&c, 0, sizeof c);
+    const int lsend = ctx->dec.global_to_local(s.send_patch);
+    c.src_base = (int64_t)lsend * ctx->g.ps;
+    c.src_is_buf = 0;
+    for (int a = 0; a < 3; ++a) {
+        c.src_lo[a] = s.send_lo[a];
+        c.dst_lo[a] = s.recv_lo[a];
+        c.size[a] = s.size[a];
+    }
+    c.nq = s.nq;
+    for (int i = 0; i < 5; ++i) c.q[i] = i < s.nq ? s.q[i] : 0;
+    c.cells = s.cells;
+    c.nelem = (int64_t)s.nq * s.cells;
+    if (to_buffer) {
+        c.dst_is_buf = 1;
+        c.dst_base = buf_base + s.offset;
+    } else {
+        const int lrecv = ctx->dec.global_to_local(s.recv_patch);
+        c.dst_is_buf = 0;
+        c.dst_base = (int64_t)lrecv * ctx->g.ps;
+    }
+    return c;
+}
+
+CopySeg buffer_to_grid(const lbm_ctx *ctx, const Seg &s, int64_t buf_base)
+{
+    CopySeg c;
+    std::memset(&c, 0, sizeof c);
+    const int lrecv = ctx->dec.global_to_local(s.recv_patch);
+    c.src_is_buf = 1;
+    c.src_base = buf_base + s.offset;
+    c.dst_is_buf = 0;
+    c.dst_base = (int64_t)lrecv * ctx->g.ps;
+    for (int a = 0; a < 3; ++a) {
+        c.dst_lo[a] = s.recv_lo[a];
+        c.size[a] = s.size[a];
+    }
+    c.nq = s.nq;
+    for (int i = 0; i < 5; ++i) c.q[i] = i < s.nq ? s.q[i] : 0;
+    c.cells = s.cells;
+    c.nelem = (int64_t)s.nq * s.cells;
+    return c;
+}
+
+// Build exchange plan, buffers and sweep boxes.
+lbm_status setup_exchange(lbm_ctx *ctx)
+{
+    build_segments(ctx->dec, ctx->segs);
+    // peers
+    std::vector<Peer> peers;
+    auto peer_of = [&](int r) -> Peer & {
+        for (Peer &p : peers)
+            if (p.rank == r) return p;
+        peers.push_back(Peer{r, 0, 0, 0, 0});
+        return peers.back();
+    };
+    for (const Seg &s : ctx->segs.send) peer_of(s.peer).send_n += (int64_t)s.nq * s.cells;
+    for (const Seg &s : ctx->segs.recv) peer_of(s.peer).recv_n += (int64_t)s.nq * s.cells;
+    std::sort(peers.begin(), peers.end(), [](const Peer &a, const Peer &b) { return a.rank < b.rank; });
+    int64_t so = 0, ro = 0;
+    for (Peer &p : peers) {
+        p.send_off = so;
+        p.recv_off = ro;
+        so += p.send_n;
+        ro += p.recv_n;
+    }
+    ctx->peers = peers;
+    ctx->send_elems = so;
+    ctx->recv_elems = ro;
+    ctx->has_remote = so > 0 || ro > 0;
+    ctx->has_nccl = false;
+    for (const Peer &p : peers)
+        if (p.rank != ctx->dec.rank) ctx->has_nccl = true;
+    lbm_status st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize);
+    if (st) return st;
+    st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize);
+    if (st) return st;
+
+    auto peer_send_off = [&](int r) {
+        for (const Peer &p : peers)
+            if (p.rank == r) return p.send_off;
+        return (int64_t)0;
+    };
+    auto peer_recv_off = [&](int r) {
+        for (const Peer &p : peers)
+            if (p.rank == r) return p.recv_off;
+        return (int64_t)0;
+    };
+    std::vector<CopySeg> pack_all, pack_remote, local, unpack;
+    for (const Seg &s : ctx->segs.send) {
+        CopySeg c = grid_to_x(ctx, s, true, peer_send_off(s.peer));
+        pack_all.push_back(c);
+        pack_remote.push_back(c);
+    }
+    for (const Seg &s : ctx->segs.local) {
+        CopySeg c = grid_to_x(ctx, s, false, 0);
+        pack_all.push_back(c);
+        local.push_back(c);
+    }
+    for (const Seg &s : ctx->segs.recv) unpack.push_back(buffer_to_grid(ctx, s, peer_recv_off(s.peer)));
+    if ((st = upload_segs(ctx, pack_all, ctx->pack_all))) return st;
+    if ((st = upload_segs(ctx, pack_remote, ctx->pack_remote))) return st;
+    if ((st = upload_segs(ctx, local, ctx->local_copy))) return st;
+    if ((st = upload_segs(ctx, unpack, ctx->unpack))) return st;
+
+    // Sweep boxes.  all: one box per local patch.  Overlap: for patches with
+    // remote segments, a shell on every side a remote segment touches (1 cell
+    // thick in y/z; SWEEP_BX thick in x so the shell rows stay coalesced) and
+    // the remaining interior box.
+    std::vector<Box> all, shell, interior;
+    const int *n = ctx->g.n;
+    const int zero[3] = {0, 0, 0};
+    std::vector<int> side(6 * ctx->dec.nlocal, 0);
+    for (const Seg &s : ctx->segs.send) {
+        const int l = ctx->dec.global_to_local(s.send_patch);
+        // s.d is the direction from the receiver to this (sending) patch; the
+        // sender's boundary layer is on side -s.d.
+        for (int a = 0; a < 3; ++a) {
+            if (s.d[a] == -1) side[6 * l + 2 * a + 1] = 1;  // high side of axis a
+            if (s.d[a] == 1) side[6 * l + 2 * a + 0] = 1;   // low side
+        }
+    }
+    for (int l = 0; l < ctx->dec.nlocal; ++l) {
+        all.push_back(make_box(l, zero, n));
+        bool any = false;
+        for (int k = 0; k < 6; ++k) any = any || side[6 * l + k];
+        if (!any) {
+            interior.push_back(make_box(l, zero, n));
+            continue;
+        }
+        int th[6];
+        for (int a = 0; a < 3; ++a) {
+            const int t = a == 0 ? SWEEP_BX : 1;
+            th[2 * a] = side[6 * l + 2 * a] ? std::min(t, n[a]) : 0;
+            th[2 * a + 1] = side[6 * l + 2 * a + 1] ? std::min(t, n[a] - th[2 * a]) : 0;
+        }
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = th[2 * a];
+            hi[a] = n[a] - th[2 * a + 1];
+        }
+        // z slabs (full xy), then y slabs (full x, inner z), then x slabs (inner y, z)
+        auto add = [&](int x0, int x1, int y0, int y1, int z0, int z1) {
+            if (x1 <= x0 || y1 <= y0 || z1 <= z0) return;
+            int blo[3] = {x0, y0, z0}, bn[3] = {x1 - x0, y1 - y0, z1 - z0};
+            shell.push_back(make_box(l, blo, bn));
+        };
+        add(0, n[0], 0, n[1], 0, lo[2]);
+        add(0, n[0], 0, n[1], hi[2], n[2]);
+        add(0, n[0], 0, lo[1], lo[2], hi[2]);
+        add(0, n[0], hi[1], n[1], lo[2], hi[2]);
+        add(0, lo[0], lo[1], hi[1], lo[2], hi[2]);
+        add(hi[0], n[0], lo[1], hi[1], lo[2], hi[2]);
+        if (hi[0] > lo[0] && hi[1] > lo[1] && hi[2] > lo[2]) {
+            int bn[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+            interior.push_back(make_box(l, lo, bn));
+        }
+    }
+    if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
+    if ((st = upload_boxes(ctx, shell, ctx->box_shell))) return st;
+    if ((st = upload_boxes(ctx, interior, ctx->box_interior))) return st;
+    ctx->use_overlap = ctx->cfg.overlap && ctx->has_nccl;
+    return LBM_OK;
+}
+
+template <typename real>
+SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
+{
+    SweepArgs<real> a;
+    a.src = (const real *)ctx->grid[ctx->cur];
+    a.dst = (real *)ctx->grid[1 - ctx->cur];
+    a.flags = ctx->flags;
+    a.kind = ctx->kind;
+    a.corr = (const real *)ctx->corr;
+    a.g = ctx->g;
+    a.omega = (real)ctx->cfg.omega;
+    a.boxes = b.boxes;
+    a.tile_prefix = b.prefix;
+    a.nboxes = b.n;
+    return a;
+}
+
+lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
+{
+    if (b.tiles == 0) return LBM_OK;
+    cudaError_t e;
+    if (ctx->esize == 8)
+        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, s);
+    else
+        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, s);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_kernel launch", __LINE__);
+    ctx->launches += 1;
+    return LBM_OK;
+}
+
+lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *grid_dst, void *buf_src, void *buf_dst,
+                       cudaStream_t s)
+{
+    if (d.n == 0 || d.max_elems == 0) return LBM_OK;
+    cudaError_t e;
+    if (ctx->esize == 8)
+        e = launch_copy_segments<double>(d.segs, d.n, d.max_elems, (const double *)grid_src, (double *)grid_dst,
+                                         (const double *)buf_src, (double *)buf_dst, ctx->g, s);
+    else
+        e = launch_copy_segments<float>(d.segs, d.n, d.max_elems, (const float *)grid_src, (float *)grid_dst,
+                                        (const float *)buf_src, (float *)buf_dst, ctx->g, s);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "copy_segments launch", __LINE__);
+    ctx->launches += (d.n + 65534) / 65535;
+    return LBM_OK;
+}
+
+// Transport of the send buffers: grouped NCCL send/recv per peer;
+// a self-peer (exchange_mode FORCE_BUFFERS) is a device copy.
+lbm_status transport(lbm_ctx *ctx, cudaStream_t s)
+{
+    const ncclDataType_t dt = ctx->esize == 8 ? ncclFloat64 : ncclFloat32;
+    char *sb = (char *)ctx->sendbuf, *rb = (char *)ctx->recvbuf;
+    for (const Peer &p : ctx->peers)
+        if (p.rank == ctx->dec.rank && p.send_n > 0)
+            CK(cudaMemcpyAsync(rb + p.recv_off * ctx->esize, sb + p.send_off * ctx->esize, p.send_n * ctx->esize,
+                               cudaMemcpyDeviceToDevice, s));
+    if (!ctx->has_nccl) return LBM_OK;
+    NK(ncclGroupStart());
+    for (const Peer &p : ctx->peers) {
+        if (p.rank == ctx->dec.rank) continue;
+        if (p.send_n > 0) NK(ncclSend(sb + p.send_off * ctx->esize, (size_t)p.send_n, dt, p.rank, ctx->nccl, s));
+        if (p.recv_n > 0) NK(ncclRecv(rb + p.recv_off * ctx->esize, (size_t)p.recv_n, dt, p.rank, ctx->nccl, s));
+    }
+    NK(ncclGroupEnd());
+    return LBM_OK;
+}
+
+// Ghost refresh of grid `gi` (used after set_pdfs / init and inside the step).
+lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts)
+{
+    void *grid = ctx->grid[gi];
+    lbm_status st;
+    if (ts) CK(cudaEventRecord(ts->ev[2], s));
+    if ((st = launch_copy(ctx, ctx->pack_all, grid, grid, nullptr, ctx->sendbuf, s))) return st;
+    if (ts) CK(cudaEventRecord(ts->ev[3], s));
+    if (ctx->has_remote) {
+        if ((st = transport(ctx, s))) return st;
+    }
+    if (ts) CK(cudaEventRecord(ts->ev[4], s));
+    if ((st = launch_copy(ctx, ctx->unpack, nullptr, grid, ctx->recvbuf, nullptr, s))) return st;
+    if (ts) CK(cudaEventRecord(ts->ev[5], s));
+    return LBM_OK;
+}
+
+lbm_status accumulate_slot(lbm_ctx *ctx, TimingSlot &ts)
+{
+    if (!ts.used) return LBM_OK;
+    CK(cudaEventSynchronize(ts.ev[kEvPerSlot - 1]));
+    auto el = [&](int a, int b) -> double {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ts.ev[a], ts.ev[b]);
+        return (double)ms;
+    };
+    if (!ts.overlap) {
+        ctx->phase_ms[PH_SWEEP] += el(1, 2);
+        ctx->phase_ms[PH_PACK] += el(2, 3);
+        ctx->phase_ms[PH_NCCL] += el(3, 4);
+        ctx->phase_ms[PH_UNPACK] += el(4, 5);
+        ctx->phase_count[PH_SWEEP] += 1;
+        ctx->phase_count[PH_PACK] += 1;
+        ctx->phase_count[PH_NCCL] += 1;
+        ctx->phase_count[PH_UNPACK] += 1;
+    } else {
+        ctx->phase_ms[PH_SHELL] += el(1, 2);
+        ctx->phase_ms[PH_PACK] += el(2, 3);
+        ctx->phase_ms[PH_NCCL] += el(6, 7);
+        ctx->phase_ms[PH_UNPACK] += el(7, 8);
+        ctx->phase_ms[PH_INTERIOR] += el(3, 9);
+        for (int p : {PH_SHELL, PH_PACK, PH_NCCL, PH_UNPACK, PH_INTERIOR}) ctx->phase_count[p] += 1;
+    }
+    ctx->phase_ms[PH_STEP] += el(0, kEvPerSlot - 1);
+    ctx->phase_count[PH_STEP] += 1;
+    ts.used = false;
+    cudaGetLastError();
+    return LBM_OK;
+}
+
+lbm_status flush_timing(lbm_ctx *ctx)
+{
+    for (int i = 0; i < kTimingSlots; ++i) {
+        lbm_status st = accumulate_slot(ctx, ctx->slots[i]);
+        if (st) return st;
+    }
+    return LBM_OK;
+}
+
+// Enqueue one time step grid[cur] -> grid[1-cur] and flip cur.
+lbm_status enqueue_step(lbm_ctx *ctx)
+{
+    cudaStream_t s = ctx->stream;
+    TimingSlot *ts = nullptr;
+    lbm_status st;
+    if (ctx->timing) {
+        ts = &ctx->slots[ctx->slot_next];
+        ctx->slot_next = (ctx->slot_next + 1) % kTimingSlots;
+        if ((st = accumulate_slot(ctx, *ts))) return st;
+        ts->used = true;
+        ts->overlap = ctx->use_overlap;
+        CK(cudaEventRecord(ts->ev[0], s));
+        CK(cudaEventRecord(ts->ev[1], s));
+    }
+    const int dsti = 1 - ctx->cur;
+    void *dst = ctx->grid[dsti];
+    if (!ctx->use_overlap) {
+        if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
+        if ((st = exchange_seq(ctx, dsti, s, ts))) return st;
+    } else {
+        cudaStream_t c = ctx->comm_stream;
+        // S: shells facing remote neighbours, then pack them.
+        if ((st = launch_sweep_set(ctx, ctx->box_shell, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[2], s));
+        if ((st = launch_copy(ctx, ctx->pack_remote, dst, dst, nullptr, ctx->sendbuf, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[3], s));
+        CK(cudaEventRecord(ts ? ts->ev[10] : ctx->slots[0].ev[10], s));
+        // C: transport + unpack while S sweeps the interiors.
+        CK(cudaStreamWaitEvent(c, ts ? ts->ev[10] : ctx->slots[0].ev[10], 0));
+        if (ts) CK(cudaEventRecord(ts->ev[6], c));
+        if ((st = transport(ctx, c))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[7], c));
+        if ((st = launch_copy(ctx, ctx->unpack, nullptr, dst, ctx->recvbuf, nullptr, c))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[8], c));
+        CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
+        if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[9], s));
+        if ((st = launch_copy(ctx, ctx->local_copy, dst, dst, nullptr, nullptr, s))) return st;
+        CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
+    }
+    if (ts) CK(cudaEventRecord(ts->ev[kEvPerSlot - 1], s));
+    ctx->cur = dsti;
+    ctx->steps += 1;
+    return LBM_OK;
+}
+
+lbm_status ensure_graph(lbm_ctx *ctx)
+{
+    const int c = ctx->cur;
+    if (ctx->graph[c]) return LBM_OK;
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = ctx->launches, s0 = ctx->steps;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    lbm_status st = enqueue_step(ctx);
+    if (!st) st = enqueue_step(ctx);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "cudaStreamEndCapture", __LINE__);
+    ctx->graph_launches[c] = ctx->launches - l0;
+    ctx->launches = l0;
+    ctx->steps = s0;  // capture did not execute anything
+    // cur flipped twice -> back to c
+    e = cudaGraphInstantiate(&ctx->graph[c], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        ctx->graph[c] = nullptr;
+        return ctx->cuda_fail(e, "cudaGraphInstantiate", __LINE__);
+    }
+    return LBM_OK;
+}
+
+lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n)
+{
+    lbm_status st;
+    const bool graphs = ctx->cfg.use_graphs && !ctx->timing;
+    while (n > 0) {
+        if (graphs && n >= 2) {
+            if ((st = ensure_graph(ctx))) return st;
+            CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
+            ctx->launches += ctx->graph_launches[ctx->cur];
+            ctx->steps += 2;
+            n -= 2;
+        } else {
+            if ((st = enqueue_step(ctx))) return st;
+            n -= 1;
+        }
+    }
+    return LBM_OK;
+}
+
+lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u, int nvel)
+{
+    const int64_t nx = ctx->dec.domain[0], ny = ctx->dec.domain[1], nz = ctx->dec.domain[2];
+    const size_t total = (size_t)(nx + 2) * (ny + 2) * (nz + 2);
+    uint8_t *dflags = nullptr;
+    lbm_status st = dev_alloc(ctx, &dflags, total);
+    if (st) return st;
+    cudaError_t e = cudaMemcpy(dflags, flags, total, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = launch_build_flags(dflags, ctx->dec.domain, ctx->dec.periodic, ctx->d_origin, ctx->dec.nlocal, ctx->g,
+                               ctx->flags, ctx->kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(dflags);
+    ctx->device_bytes -= (int64_t)total;
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "build flags", __LINE__);
+    ctx->launches += 2 * ((ctx->dec.nlocal + 65534) / 65535);
+    // Wall correction table 6 w_i rho0 (e_i . u_w[k]) (R3, R9),
+    // computed in double and rounded once to the storage precision.
+    std::vector<double> cd((size_t)LBM_MAX_WALL_VELOCITIES * Q, 0.0);
+    for (int k = 0; k < nvel; ++k)
+        for (int i = 0; i < Q; ++i) {
+            const double eu = EX(i) * wall_u[3 * k] + EY(i) * wall_u[3 * k + 1] + EZ(i) * wall_u[3 * k + 2];
+            cd[(size_t)k * Q + i] = 6.0 * WQ(i) * 1.0 * eu;
+        }
+    if (ctx->esize == 8) {
+        CK(cudaMemcpy(ctx->corr, cd.data(), cd.size() * sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> cf(cd.begin(), cd.end());
+        CK(cudaMemcpy(ctx->corr, cf.data(), cf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    // Fluid cell counts (MFLUPS counts fluid cells, R16).
+    int64_t gl = 0, lo = 0;
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y) {
+            const uint8_t *row = flags + ((z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + 1;
+            const bool zy_owned = z >= ctx->dec.owned_lo[2] && z < ctx->dec.owned_hi[2] && y >= ctx->dec.owned_lo[1] &&
+                                  y < ctx->dec.owned_hi[1];
+            for (int64_t x = 0; x < nx; ++x) {
+                if (row[x] == 0) {
+                    ++gl;
+                    if (zy_owned && x >= ctx->dec.owned_lo[0] && x < ctx->dec.owned_hi[0]) ++lo;
+                }
+            }
+        }
+    ctx->fluid_global = gl;
+    ctx->fluid_local = lo;
+    ctx->flags_set = true;
+    return LBM_OK;
+}
+
+const char *validate_flags(const Decomp &dec, const uint8_t *flags, const double *wall_u, int nvel)
+{
+    static thread_local char msg[256];
+    if (!flags) return "flags is NULL";
+    if (nvel < 0 || nvel > LBM_MAX_WALL_VELOCITIES) return "nvel must be in [0, 254]";
+    if (nvel > 0 && !wall_u) return "wall_u is NULL but nvel > 0";
+    for (int k = 0; k < 3 * nvel; ++k)
+        if (!std::isfinite(wall_u[k])) return "wall_u must be finite";
+    const int64_t nx = dec.domain[0], ny = dec.domain[1], nz = dec.domain[2];
+    for (int64_t z = -1; z <= nz; ++z)
+        for (int64_t y = -1; y <= ny; ++y) {
+            const uint8_t *row = flags + ((z + 1) * (ny + 2) + (y + 1)) * (nx + 2);
+            const bool yz_shell = (!dec.periodic[1] && (y < 0 || y >= ny)) || (!dec.periodic[2] && (z < 0 || z >= nz));
+            for (int64_t x = -1; x <= nx; ++x) {
+                const uint8_t f = row[x + 1];
+                const bool shell = yz_shell || (!dec.periodic[0] && (x < 0 || x >= nx));
+                if (shell && f == LBM_FLUID) {
+                    std::snprintf(msg, sizeof msg, "shell cell (%lld,%lld,%lld) on a non-periodic axis is fluid",
+                                  (long long)x, (long long)y, (long long)z);
+                    return msg;
+                }
+                if (f >= LBM_VELOCITY0 && f - LBM_VELOCITY0 >= nvel) {
+                    std::snprintf(msg, sizeof msg, "cell (%lld,%lld,%lld) has velocity wall %d but nvel = %d",
+                                  (long long)x, (long long)y, (long long)z, f - LBM_VELOCITY0, nvel);
+                    return msg;
+                }
+            }
+        }
+    return "";
+}
+
+void destroy_ctx(lbm_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+    for (int i = 0; i < 2; ++i)
+        if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
+    if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
+                    ctx->recvbuf, ctx->pack_all.segs, ctx->pack_remote.segs, ctx->local_copy.segs, ctx->unpack.segs,
+                    ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
+                    ctx->box_interior.boxes, ctx->box_interior.prefix};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->events_created)
+        for (auto &sl : ctx->slots)
+            for (auto &ev : sl.ev) cudaEventDestroy(ev);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    cudaGetLastError();
+    delete ctx;
+}
+
+lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
+{
+    if (!out) return LBM_ERR_ARG;
+    *out = nullptr;
+    if (!cfg) {
+        g_create_error = "cfg is NULL";
+        return LBM_ERR_ARG;
+    }
+    Decomp dec;
+    const char *m = decompose(*cfg, dec);
+    if (m[0]) {
+        g_create_error = m;
+        return LBM_ERR_ARG;
+    }
+    if (cfg->nranks > 1 && !cfg->nccl_unique_id) {
+        g_create_error = "nccl_unique_id is required when nranks > 1";
+        return LBM_ERR_ARG;
+    }
+    lbm_ctx *ctx = new (std::nothrow) lbm_ctx();
+    if (!ctx) {
+        g_create_error = "host allocation failed";
+        return LBM_ERR_OOM;
+    }
+    ctx->cfg = *cfg;
+    ctx->dec = dec;
+    ctx->esize = cfg->precision;
+    if (const char *a = std::getenv("LBM_ALIGN_BYTES")) {
+        int v = std::atoi(a);
+        if (v >= ctx->esize && v <= 1024 && (v & (v - 1)) == 0) ctx->align = v;
+    }
+    auto bail = [&](lbm_status st) {
+        g_create_error = ctx->err.empty() ? "create failed" : ctx->err;
+        destroy_ctx(ctx);
+        return st;
+    };
+    // Device
+    int dev = cfg->device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+            return bail(LBM_ERR_CUDA);
+        }
+    }
+    ctx->device = dev;
+    {
+        cudaError_t e = cudaSetDevice(dev);
+        cudaDeviceProp prop;
+        if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cannot use CUDA device: ") + cudaGetErrorString(e);
+            cudaGetLastError();
+            return bail(LBM_ERR_CUDA);
+        }
+        if (prop.major != 10 || prop.minor != 0) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "liblbm_b200 is built for sm_100a (B200); device %d is %s (sm_%d%d)", dev,
+                          prop.name, prop.major, prop.minor);
+            ctx->err = buf;
+            return bail(LBM_ERR_CUDA);
+        }
+    }
+    ctx->g = make_geom(dec.patch, ctx->esize, ctx->align);
+    lbm_status st;
+    // Streams and events
+    if (cfg->stream) {
+        ctx->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate failed";
+            return bail(LBM_ERR_CUDA);
+        }
+        ctx->own_stream = true;
+    }
+    if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        ctx->err = "cudaStreamCreate failed";
+        return bail(LBM_ERR_CUDA);
+    }
+    for (auto &sl : ctx->slots)
+        for (auto &ev : sl.ev)
+            if (cudaEventCreate(&ev) != cudaSuccess) {
+                ctx->err = "cudaEventCreate failed";
+                return bail(LBM_ERR_CUDA);
+            }
+    ctx->events_created = true;
+    // Memory budget check (clean OOM before the big allocations).
+    const size_t grid_bytes = (size_t)dec.nlocal * ctx->g.ps * ctx->esize;
+    const size_t flag_bytes = (size_t)dec.nlocal * ctx->g.fs;
+    {
+        size_t freeb = 0, totalb = 0;
+        if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess && 2 * grid_bytes + 2 * flag_bytes > freeb) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "need %.2f GB of device memory for the PDF grids and flags, %.2f GB free",
+                          (2.0 * grid_bytes + 2.0 * flag_bytes) / 1e9, freeb / 1e9);
+            ctx->err = buf;
+            return bail(LBM_ERR_OOM);
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        if ((st = dev_alloc(ctx, &ctx->grid[i], grid_bytes))) return bail(st);
+        if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
+    }
+    if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->corr, (size_t)LBM_MAX_WALL_VELOCITIES * Q * ctx->esize))) return bail(st);
+    {
+        std::vector<int> origin(3 * dec.nlocal);
+        for (int l = 0; l < dec.nlocal; ++l) {
+            int c[3];
+            dec.patch_coord(dec.local_to_global(l), c);
+            for (int a = 0; a < 3; ++a) origin[3 * l + a] = c[a] * dec.patch[a];
+        }
+        if ((st = dev_alloc(ctx, &ctx->d_origin, origin.size() * sizeof(int)))) return bail(st);
+        if (cudaMemcpy(ctx->d_origin, origin.data(), origin.size() * sizeof(int), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+            return bail(LBM_ERR_CUDA);
+    }
+    if ((st = setup_exchange(ctx))) return bail(st);
+    // NCCL communicator (bootstrap id broadcast by the caller, e.g. torch.distributed)
+    if (cfg->nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->nccl, cfg->nranks, id, cfg->rank);
+        if (r != ncclSuccess) {
+            ctx->nccl = nullptr;
+            ctx->err = std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r);
+            return bail(LBM_ERR_NCCL);
+        }
+    }
+    // Default geometry: closed no-slip box at rest (f~ = 0).
+    {
+        const int64_t nx = dec.domain[0], ny = dec.domain[1], nz = dec.domain[2];
+        std::vector<uint8_t> fl((size_t)(nx + 2) * (ny + 2) * (nz + 2), 0);
+        for (int64_t z = -1; z <= nz; ++z)
+            for (int64_t y = -1; y <= ny; ++y)
+                for (int64_t x = -1; x <= nx; ++x) {
+                    const bool shell = x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz;
+                    if (shell) fl[((z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + (x + 1)] = LBM_NOSLIP;
+                }
+        if ((st = apply_flags(ctx, fl.data(), nullptr, 0))) return bail(st);
+    }
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
+    *out = ctx;
+    return LBM_OK;
+}
+
+// Staging for host <-> device transfers of the canonical layout.
+constexpr size_t kStageBytes = (size_t)256 << 20;
+
+lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode, double *rho, double *u)
+{
+    const int64_t on[3] = {ctx->dec.owned_hi[0] - ctx->dec.owned_lo[0], ctx->dec.owned_hi[1] - ctx->dec.owned_lo[1],
+                           ctx->dec.owned_hi[2] - ctx->dec.owned_lo[2]};
+    const int64_t plane_cells = on[0] * on[1];
+    const size_t per_cell = mode == 0 ? Q * sizeof(double) : 4 * sizeof(double);
+    int64_t zc = (int64_t)(kStageBytes / (plane_cells * per_cell));
+    if (zc < 1) zc = 1;
+    if (zc > on[2]) zc = on[2];
+    double *stage = nullptr;
+    lbm_status st = dev_alloc(ctx, &stage, (size_t)zc * plane_cells * per_cell);
+    if (st) return st;
+    const void *grid = ctx->grid[ctx->cur];
+    cudaError_t e = cudaSuccess;
+    for (int64_t z0 = 0; z0 < on[2] && e == cudaSuccess; z0 += zc) {
+        const int64_t nzc = std::min(zc, on[2] - z0);
+        const size_t cells = (size_t)(nzc * plane_cells);
+        if (to_device) {
+            e = cudaMemcpyAsync(stage, host + (size_t)z0 * plane_cells * Q, cells * Q * sizeof(double),
+                                cudaMemcpyHostToDevice, ctx->stream);
+            if (e == cudaSuccess)
+                e = ctx->esize == 8 ? launch_import<double>(stage, z0, nzc, ctx->dec.owned_lo, on, ctx->dec.brick,
+                                                            ctx->g, (double *)grid, ctx->stream)
+                                    : launch_import<float>(stage, z0, nzc, ctx->dec.owned_lo, on, ctx->dec.brick,
+                                                           ctx->g, (float *)grid, ctx->stream);
+            ctx->launches += 1;
+        } else {
+            double *srho = stage, *su = stage + cells;
+            e = ctx->esize == 8
+                    ? launch_export<double>((const double *)grid, ctx->flags, z0, nzc, ctx->dec.owned_lo, on,
+                                            ctx->dec.brick, ctx->g, stage, mode, srho, su, ctx->stream)
+                    : launch_export<float>((const float *)grid, ctx->flags, z0, nzc, ctx->dec.owned_lo, on,
+                                           ctx->dec.brick, ctx->g, stage, mode, srho, su, ctx->stream);
+            ctx->launches += 1;
+            if (e == cudaSuccess) {
+                if (mode == 0) {
+                    e = cudaMemcpyAsync(host + (size_t)z0 * plane_cells * Q, stage, cells * Q * sizeof(double),
+                                        cudaMemcpyDeviceToHost, ctx->stream);
+                } else {
+                    if (rho)
+                        e = cudaMemcpyAsync(rho + (size_t)z0 * plane_cells, srho, cells * sizeof(double),
+                                            cudaMemcpyDeviceToHost, ctx->stream);
+                    if (e == cudaSuccess && u)
+                        e = cudaMemcpyAsync(u + (size_t)z0 * plane_cells * 3, su, cells * 3 * sizeof(double),
+                                            cudaMemcpyDeviceToHost, ctx->stream);
+                }
+            }
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    }
+    cudaFree(stage);
+    ctx->device_bytes -= (int64_t)((size_t)zc * plane_cells * per_cell);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "host/device transfer", __LINE__);
+    return LBM_OK;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+LBM_API int32_t lbm_abi_version(void) { return LBM_ABI_VERSION; }
+
+LBM_API void lbm_config_default(lbm_config *cfg)
+{
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->omega = 1.0 / 0.65;
+    cfg->precision = LBM_FP64;
+    cfg->device = -1;
+    cfg->rank = 0;
+    cfg->nranks = 1;
+    cfg->exchange_mode = LBM_EXCHANGE_AUTO;
+    cfg->overlap = 1;
+    cfg->use_graphs = 1;
+}
+
+LBM_API lbm_status lbm_create(const int64_t domain[3], const int32_t patch[3], double omega, int32_t precision,
+                              lbm_ctx **out)
+{
+    if (!domain || !patch) {
+        g_create_error = "domain/patch is NULL";
+        if (out) *out = nullptr;
+        return LBM_ERR_ARG;
+    }
+    lbm_config cfg;
+    lbm_config_default(&cfg);
+    for (int a = 0; a < 3; ++a) {
+        cfg.domain[a] = domain[a];
+        cfg.patch[a] = patch[a];
+    }
+    cfg.omega = omega;
+    cfg.precision = precision;
+    return create_impl(&cfg, out);
+}
+
+LBM_API lbm_status lbm_create_ex(const lbm_config *cfg, lbm_ctx **out) { return create_impl(cfg, out); }
+
+LBM_API lbm_status lbm_destroy(lbm_ctx *ctx)
+{
+    destroy_ctx(ctx);
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_set_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u, int32_t nvel)
+{
+    CHECK_CTX(ctx);
+    const char *m = validate_flags(ctx->dec, flags, wall_u, nvel);
+    if (m[0]) return ctx->fail(LBM_ERR_ARG, m);
+    CK(cudaStreamSynchronize(ctx->stream));
+    return apply_flags(ctx, flags, wall_u, nvel);
+}
+
+LBM_API lbm_status lbm_get_flags(lbm_ctx *ctx, uint8_t *out)
+{
+    CHECK_CTX(ctx);
+    if (!out) return ctx->fail(LBM_ERR_ARG, "flags_out is NULL");
+    CK(cudaStreamSynchronize(ctx->stream));
+    const Decomp &d = ctx->dec;
+    const Geom &g = ctx->g;
+    std::vector<uint8_t> h((size_t)d.nlocal * g.fs);
+    CK(cudaMemcpy(h.data(), ctx->flags, h.size(), cudaMemcpyDeviceToHost));
+    const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
+    for (int64_t z = -1; z <= on[2]; ++z)
+        for (int64_t y = -1; y <= on[1]; ++y)
+            for (int64_t x = -1; x <= on[0]; ++x) {
+                const int64_t c[3] = {x, y, z};
+                int b[3], lc[3];
+                for (int a = 0; a < 3; ++a) {
+                    int64_t cc = std::min(std::max(c[a], (int64_t)0), on[a] - 1);
+                    b[a] = (int)(cc / g.n[a]);
+                    lc[a] = (int)(c[a] - (int64_t)b[a] * g.n[a]);
+                }
+                const int lp = (b[2] * d.brick[1] + b[1]) * d.brick[0] + b[0];
+                const int64_t ci = ((int64_t)(lc[2] + 1) * g.py + (lc[1] + 1)) * g.px + (lc[0] + g.xo);
+                out[((z + 1) * (on[1] + 2) + (y + 1)) * (on[0] + 2) + (x + 1)] = h[(size_t)lp * g.fs + ci];
+            }
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_set_pdfs(lbm_ctx *ctx, const double *f)
+{
+    CHECK_CTX(ctx);
+    if (!f) return ctx->fail(LBM_ERR_ARG, "f is NULL");
+    CK(cudaStreamSynchronize(ctx->stream));
+    lbm_status st = transfer_chunks(ctx, const_cast<double *>(f), true, 0, nullptr, nullptr);
+    if (st) return st;
+    if ((st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr))) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_init_noise(lbm_ctx *ctx, uint64_t seed)
+{
+    CHECK_CTX(ctx);
+    const Decomp &d = ctx->dec;
+    const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
+    cudaError_t e = ctx->esize == 8
+                        ? launch_noise<double>((double *)ctx->grid[ctx->cur], seed, d.domain, d.owned_lo, on, d.brick,
+                                               ctx->g, ctx->stream)
+                        : launch_noise<float>((float *)ctx->grid[ctx->cur], seed, d.domain, d.owned_lo, on, d.brick,
+                                              ctx->g, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "noise_kernel", __LINE__);
+    ctx->launches += 1;
+    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr);
+    if (st) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_step_async(lbm_ctx *ctx, int64_t nsteps)
+{
+    CHECK_CTX(ctx);
+    if (nsteps < 0) return ctx->fail(LBM_ERR_ARG, "nsteps must be >= 0");
+    return enqueue_steps(ctx, nsteps);
+}
+
+LBM_API lbm_status lbm_synchronize(lbm_ctx *ctx)
+{
+    CHECK_CTX(ctx);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->comm_stream));
+    if (ctx->timing) return flush_timing(ctx);
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_step(lbm_ctx *ctx, int64_t nsteps)
+{
+    lbm_status st = lbm_step_async(ctx, nsteps);
+    if (st) return st;
+    return lbm_synchronize(ctx);
+}
+
+LBM_API lbm_status lbm_get_pdfs(lbm_ctx *ctx, double *f_out)
+{
+    CHECK_CTX(ctx);
+    if (!f_out) return ctx->fail(LBM_ERR_ARG, "f_out is NULL");
+    CK(cudaStreamSynchronize(ctx->stream));
+    return transfer_chunks(ctx, f_out, false, 0, nullptr, nullptr);
+}
+
+LBM_API lbm_status lbm_get_pdfs_at(lbm_ctx *ctx, const int64_t *xyz, int64_t n, double *out)
+{
+    CHECK_CTX(ctx);
+    if (n < 0 || (n > 0 && (!xyz || !out))) return ctx->fail(LBM_ERR_ARG, "bad sample arguments");
+    if (n == 0) return LBM_OK;
+    std::vector<int64_t> loc((size_t)3 * n);
+    for (int64_t k = 0; k < n; ++k)
+        for (int a = 0; a < 3; ++a) {
+            const int64_t c = xyz[3 * k + a];
+            if (c < ctx->dec.owned_lo[a] || c >= ctx->dec.owned_hi[a])
+                return ctx->fail(LBM_ERR_ARG, "sample cell outside the owned brick");
+            loc[3 * k + a] = c - ctx->dec.owned_lo[a];
+        }
+    int64_t *dxyz = nullptr;
+    double *dout = nullptr;
+    lbm_status st = dev_alloc(ctx, &dxyz, loc.size() * sizeof(int64_t));
+    if (st) return st;
+    st = dev_alloc(ctx, &dout, (size_t)n * Q * sizeof(double));
+    if (st) {
+        cudaFree(dxyz);
+        return st;
+    }
+    cudaError_t e = cudaMemcpyAsync(dxyz, loc.data(), loc.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+        e = ctx->esize == 8 ? launch_gather<double>((const double *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
+                                                    ctx->dec.brick, ctx->g, dout, ctx->stream)
+                            : launch_gather<float>((const float *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
+                                                   ctx->dec.brick, ctx->g, dout, ctx->stream);
+    ctx->launches += 1;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, dout, (size_t)n * Q * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(dxyz);
+    cudaFree(dout);
+    ctx->device_bytes -= (int64_t)(loc.size() * sizeof(int64_t) + (size_t)n * Q * sizeof(double));
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "gather", __LINE__);
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho_out, double *u_out)
+{
+    CHECK_CTX(ctx);
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!rho_out && !u_out) return LBM_OK;
+    return transfer_chunks(ctx, nullptr, false, 1, rho_out, u_out);
+}
+
+static void fill_info_decomp(const Decomp &d, int esize, const SegLists &segs, lbm_info *out)
+{
+    for (int a = 0; a < 3; ++a) {
+        out->domain[a] = d.domain[a];
+        out->patch[a] = d.patch[a];
+        out->proc_grid[a] = d.proc[a];
+        out->proc_coord[a] = d.coord[a];
+        out->owned_lo[a] = d.owned_lo[a];
+        out->owned_hi[a] = d.owned_hi[a];
+    }
+    out->precision = esize;
+    out->rank = d.rank;
+    out->nranks = d.nranks;
+    out->patches_local = d.nlocal;
+    out->patches_global = d.pgrid[0] * d.pgrid[1] * d.pgrid[2];
+    std::vector<int> peers;
+    int64_t remote = 0, local = 0;
+    int msgs = 0;
+    for (const Seg &s : segs.send) {
+        if (s.peer != d.rank) {
+            remote += (int64_t)s.nq * s.cells * esize;
+            ++msgs;
+            if (std::find(peers.begin(), peers.end(), s.peer) == peers.end()) peers.push_back(s.peer);
+        } else {
+            local += (int64_t)s.nq * s.cells * esize;
+        }
+    }
+    for (const Seg &s : segs.local) local += (int64_t)s.nq * s.cells * esize;
+    out->peers = (int32_t)peers.size();
+    out->messages_remote = msgs;
+    out->halo_bytes_remote_per_step = remote;
+    out->halo_bytes_local_per_step = local;
+}
+
+LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
+{
+    if (!ctx || !out) return LBM_ERR_ARG;
+    std::memset(out, 0, sizeof *out);
+    fill_info_decomp(ctx->dec, ctx->esize, ctx->segs, out);
+    out->fluid_cells_local = ctx->fluid_local;
+    out->fluid_cells_global = ctx->fluid_global;
+    out->steps_done = ctx->steps;
+    out->bytes_per_step_algorithmic = 2.0 * Q * ctx->esize * (double)ctx->fluid_local;
+    out->kernel_launches = ctx->launches;
+    out->device_bytes = ctx->device_bytes;
+    for (int i = 0; i < LBM_NPHASES; ++i) {
+        out->phase_ms[i] = ctx->phase_ms[i];
+        out->phase_count[i] = ctx->phase_count[i];
+    }
+    out->row_pitch_elems = ctx->g.px;
+    out->align_bytes = ctx->align;
+    out->graphs_active = (ctx->graph[0] || ctx->graph[1]) ? 1 : 0;
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_set_timing(lbm_ctx *ctx, int32_t enable)
+{
+    CHECK_CTX(ctx);
+    CK(cudaStreamSynchronize(ctx->stream));
+    lbm_status st = flush_timing(ctx);
+    if (st) return st;
+    ctx->timing = enable != 0;
+    for (int i = 0; i < LBM_NPHASES; ++i) {
+        ctx->phase_ms[i] = 0;
+        ctx->phase_count[i] = 0;
+    }
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_get_stream(lbm_ctx *ctx, void **stream_out)
+{
+    if (!ctx || !stream_out) return LBM_ERR_ARG;
+    *stream_out = (void *)ctx->stream;
+    return LBM_OK;
+}
+
+LBM_API const char *lbm_last_error(const lbm_ctx *ctx)
+{
+    if (!ctx) return g_create_error.c_str();
+    return ctx->err.c_str();
+}
+
+LBM_API lbm_status lbm_nccl_unique_id(void *out, int64_t nbytes)
+{
+    if (!out || nbytes < (int64_t)sizeof(ncclUniqueId)) return LBM_ERR_ARG;
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_create_error = std::string("ncclGetUniqueId failed: ") + ncclGetErrorString(r);
+        return LBM_ERR_NCCL;
+    }
+    std::memcpy(out, &id, sizeof id);
+    return LBM_OK;
+}
+
+LBM_API lbm_status lbm_plan(const lbm_config *cfg, lbm_info *info, lbm_msg *msgs, int32_t cap, int32_t *nmsgs)
+{
+    if (!cfg) return LBM_ERR_ARG;
+    Decomp dec;
+    const char *m = decompose(*cfg, dec);
+    if (m[0]) {
+        g_create_error = m;
+        return LBM_ERR_ARG;
+    }
+    SegLists segs;
+    build_segments(dec, segs);
+    if (info) {
+        std::memset(info, 0, sizeof *info);
+        fill_info_decomp(dec, cfg->precision, segs, info);
+    }
+    int32_t k = 0;
+    auto emit = [&](const Seg &s, int send) {
+        if (s.peer == dec.rank && !dec.force_buffers) return;
+        if (msgs && k < cap) {
+            lbm_msg &o = msgs[k];
+            o.peer = s.peer;
+            o.send = send;
+            o.patch_local = send ? s.send_patch : s.recv_patch;
+            o.patch_remote = send ? s.recv_patch : s.send_patch;
+            for (int a = 0; a < 3; ++a) o.dir[a] = s.d[a];
+            o.nq = s.nq;
+            o.cells = s.cells;
+            o.offset = s.offset;
+        }
+        ++k;
+    };
+    for (const Seg &s : segs.send) emit(s, 1);
+    for (const Seg &s : segs.recv) emit(s, 0);
+    if (nmsgs) *nmsgs = k;
+    return LBM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): max |f~_GPU - f~_oracle| <= 1e-12 (fp64)
+and <= 1e-5 (fp32, fp32 storage and arithmetic vs the fp64 oracle, R15) over
+fluid cells; flags, fluid-cell counts and non-fluid rho/u bit-exact;
+multi-patch / forced-buffer / graph variants bitwise equal to single patch.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1007_1388_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = {8: 1e-12, 4: 1e-5}
+
+
+def lbm():
+    from paper_1007_1388_b200 import lbm as m
+    return m
+
+
+def fluid_mask(flags):
+    return flags[1:-1, 1:-1, 1:-1] == 0
+
+
+def max_fluid_diff(a, b, flags):
+    m = fluid_mask(flags)
+    return float(np.abs(a[m] - b[m]).max()) if m.any() else 0.0
+
+
+def run_gpu(domain, flags, wall_u, f0, steps, prec=8, patch=None, omega=inputs.LDC_OMEGA, **kw):
+    L = lbm().Lattice(domain, patch or domain, omega, prec, **kw)
+    try:
+        L.set_flags(flags, wall_u)
+        L.set_pdfs(f0)
+        L.step(steps)
+        return L.get_pdfs()
+    finally:
+        L.close()
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_ldc_32_100_steps_vs_oracle(prec):
+    """BASELINE configs[0]: LDC 32^3, single patch, 100 steps, dyadic noise init."""
+    n = (32, 32, 32)
+    fl, wu = inputs.ldc_flags(n)
+    f0 = inputs.noise_pdfs(n)
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 100, nthreads=oracle.max_threads())
+    got = run_gpu(n, fl, wu, f0, 100, prec)
+    d = max_fluid_diff(got, ref, fl)
+    assert d <= TOL[prec], d
+    # non-fluid cells read back as 0 (R13)
+    assert np.all(got[~fluid_mask(fl)] == 0.0)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_ragged_obstacles_two_lids_periodic_x(prec):
+    """Ragged sizes (not multiples of the 64 x 4 tile), interior obstacles, two moving
+    walls, periodic x: 30 steps."""
+    n = (37, 29, 23)
+    fl, wu = inputs.ldc_flags(n, periodic=(1, 0, 0))
+    fl = inputs.add_obstacles(fl, 0.08, seed=5, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.0, -0.02, 0.01]]])
+    f0 = inputs.noise_pdfs(n, seed=11)
+    ref = oracle.run(f0, fl, wu, 1.3, 30, periodic=(1, 0, 0), nthreads=oracle.max_threads())
+    got = run_gpu(n, fl, wu, f0, 30, prec, omega=1.3, periodic=(1, 0, 0))
+    assert max_fluid_diff(got, ref, fl) <= TOL[prec]
+
+
+def test_fully_periodic_single_patch_self_exchange():
+    """A periodic single patch is its own neighbour in all 18 directions."""
+    n = (16, 12, 8)
+    fl = np.zeros((n[2] + 2, n[1] + 2, n[0] + 2), np.uint8)
+    f0 = inputs.noise_pdfs(n, seed=3)
+    ref = oracle.run(f0, fl, np.zeros((0, 3)), 1.7, 40, periodic=(1, 1, 1))
+    got = run_gpu(n, fl, None, f0, 40, 8, omega=1.7, periodic=(1, 1, 1))
+    assert max_fluid_diff(got, ref, fl) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_multi_patch_bitwise_equal_single_patch(prec):
+    """Decomposition invariance: 3x3x3 ragged patches with
+    periodic y, obstacles; bitwise equal to one patch, within tolerance of the oracle."""
+    n = (36, 30, 24)
+    fl, wu = inputs.ldc_flags(n, periodic=(0, 1, 0))
+    fl = inputs.add_obstacles(fl, 0.05, seed=9)
+    f0 = inputs.noise_pdfs(n, seed=21)
+    one = run_gpu(n, fl, wu, f0, 25, prec, periodic=(0, 1, 0))
+    many = run_gpu(n, fl, wu, f0, 25, prec, patch=(12, 10, 8), periodic=(0, 1, 0))
+    forced = run_gpu(n, fl, wu, f0, 25, prec, patch=(12, 10, 8), periodic=(0, 1, 0),
+                     exchange_mode=lbm().LBM_EXCHANGE_FORCE_BUFFERS)
+    np.testing.assert_array_equal(many, one)
+    np.testing.assert_array_equal(forced, one)
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 25, periodic=(0, 1, 0), nthreads=oracle.max_threads())
+    assert max_fluid_diff(one, ref, fl) <= TOL[prec]
+
+
+def test_graphs_and_odd_steps_bitwise():
+    n = (20, 18, 16)
+    fl, wu = inputs.ldc_flags(n)
+    f0 = inputs.noise_pdfs(n, seed=2)
+    a = run_gpu(n, fl, wu, f0, 7, 8, patch=(10, 9, 8), use_graphs=1)
+    b = run_gpu(n, fl, wu, f0, 7, 8, patch=(10, 9, 8), use_graphs=0)
+    np.testing.assert_array_equal(a, b)
+    # 7 = 3 + 4 via separate calls
+    L = lbm().Lattice(n, (10, 9, 8))
+    L.set_flags(fl, wu)
+    L.set_pdfs(f0)
+    L.step(3)
+    L.step(4)
+    np.testing.assert_array_equal(L.get_pdfs(), a)
+    L.close()
+
+
+@pytest.mark.parametrize("i", range(19))
+def test_impulse_each_direction(i):
+    """Hand-derivable single-PDF impulses (U = 0): one step moves f~_i(x0) to x0 + e_i
+    or bounces it back at a wall; compared with the oracle at every cell."""
+    n = (5, 5, 5)
+    fl = inputs.shell_flags(n)
+    for x0 in [(2, 2, 2), (0, 0, 0), (4, 0, 4), (0, 4, 2)]:
+        f0 = np.zeros((5, 5, 5, 19))
+        f0[x0[2], x0[1], x0[0], i] = 1e-3
+        ref = oracle.run(f0, fl, np.zeros((0, 3)), 1.5, 1)
+        got = run_gpu(n, fl, None, f0, 1, 8, omega=1.5)
+        assert max_fluid_diff(got, ref, fl) <= 1e-18
+
+
+def test_device_noise_init_matches_generator():
+    """lbm_init_noise draws the same dyadic values as inputs.noise_pdfs (bitwise, both precisions)."""
+    n = (20, 12, 9)
+    expect = inputs.noise_pdfs(n, seed=1388)
+    for prec in (8, 4):
+        L = lbm().Lattice(n, (10, 6, 9), 1.0, prec, periodic=(1, 1, 1))
+        L.set_flags(np.zeros((11, 14, 22), np.uint8))
+        L.init_noise(1388)
+        np.testing.assert_array_equal(L.get_pdfs(), expect)
+        L.close()
+
+
+def test_flags_readback_and_fluid_count_bit_exact():
+    n = (24, 16, 12)
+    fl, wu = inputs.ldc_flags(n)
+    fl = inputs.add_obstacles(fl, 0.1, seed=4)
+    L = lbm().Lattice(n, (12, 8, 6))
+    L.set_flags(fl, wu)
+    np.testing.assert_array_equal(L.get_flags(), fl)
+    info = L.info()
+    assert info["fluid_cells_global"] == int(fluid_mask(fl).sum()) == info["fluid_cells_local"]
+    assert info["bytes_per_step_algorithmic"] == 2 * 19 * 8 * info["fluid_cells_local"]
+    L.close()
+
+
+def test_macroscopic_vs_oracle():
+    n = (16, 16, 16)
+    fl, wu = inputs.ldc_flags(n)
+    fl = inputs.add_obstacles(fl, 0.05, seed=8)
+    f0 = inputs.noise_pdfs(n)
+    L = lbm().Lattice(n, (8, 8, 8))
+    L.set_flags(fl, wu)
+    L.set_pdfs(f0)
+    L.step(50)
+    rho, u = L.get_macroscopic()
+    f = L.get_pdfs()
+    L.close()
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 50)
+    rr, ur = oracle.macroscopic(ref, fl)
+    m = fluid_mask(fl)
+    assert np.abs(rho[m] - rr[m]).max() <= 1e-12
+    assert np.abs(u[m] - ur[m]).max() <= 1e-12
+    assert np.all(rho[~m] == 0.0) and np.all(u[~m] == 0.0)
+    # and the exported moments are those of the exported PDFs
+    r2, u2 = oracle.macroscopic(f, fl)
+    assert np.abs(rho - r2).max() <= 1e-15
+
+
+def test_default_state_closed_box_at_rest():
+    """After create: closed no-slip box at rest; stepping keeps it exactly zero."""
+    L = lbm().Lattice((9, 7, 5), minimal=True)
+    L.step(5)
+    assert np.all(L.get_pdfs() == 0.0)
+    assert L.info()["fluid_cells_global"] == 9 * 7 * 5
+    L.close()
+
+
+def test_edge_cases():
+    m = lbm()
+    # 1x1x1 fluid cell in a closed box; only rest + bounce-back
+    n = (1, 1, 1)
+    fl = inputs.shell_flags(n)
+    f0 = inputs.noise_pdfs(n)
+    ref = oracle.run(f0, fl, np.zeros((0, 3)), 1.2, 5)
+    got = run_gpu(n, fl, None, f0, 5, 8, omega=1.2)
+    assert max_fluid_diff(got, ref, fl) <= 1e-15
+    # no fluid at all: step is a no-op, output zeros
+    n = (6, 5, 4)
+    fl = np.ones((6, 7, 8), np.uint8)
+    L = m.Lattice(n)
+    L.set_flags(fl)
+    L.set_pdfs(inputs.noise_pdfs(n))
+    L.step(3)
+    assert np.all(L.get_pdfs() == 0.0) and L.info()["fluid_cells_global"] == 0
+    # invalid flags leave the state unchanged
+    fl_ok, wu = inputs.ldc_flags(n)
+    L.set_flags(fl_ok, wu)
+    bad = fl_ok.copy()
+    bad[0, 2, 2] = 0  # fluid shell cell on non-periodic z
+    with pytest.raises(m.LbmError) as ei:
+        L.set_flags(bad, wu)
+    assert ei.value.status == 1
+    with pytest.raises(m.LbmError):
+        L.set_flags(fl_ok, None)  # velocity wall without a velocity table
+    np.testing.assert_array_equal(L.get_flags(), fl_ok)
+    with pytest.raises(m.LbmError):
+        L.step(-1)
+    L.step(0)
+    L.close()
+    # nx = 1 rows, thin patches
+    n = (1, 7, 9)
+    fl, wu = inputs.ldc_flags(n, periodic=(1, 0, 0))
+    f0 = inputs.noise_pdfs(n)
+    ref = oracle.run(f0, fl, wu, 1.1, 12, periodic=(1, 0, 0))
+    got = run_gpu(n, fl, wu, f0, 12, 8, omega=1.1, patch=(1, 7, 3), periodic=(1, 0, 0))
+    assert max_fluid_diff(got, ref, fl) <= 1e-13
+
+
+def test_sampled_cells_api():
+    n = (16, 8, 8)
+    L = lbm().Lattice(n, (8, 8, 8), 1.0, 8, periodic=(1, 1, 1))
+    L.set_flags(np.zeros((10, 10, 18), np.uint8))
+    L.init_noise(5)
+    cells = [(0, 0, 0), (15, 7, 7), (8, 3, 4)]
+    np.testing.assert_array_equal(L.get_pdfs_at(cells), inputs.noise_at(n, cells, seed=5))
+    with pytest.raises(lbm().LbmError):
+        L.get_pdfs_at([(16, 0, 0)])
+    L.close()
