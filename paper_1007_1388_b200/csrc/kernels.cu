@@ -27,10 +27,13 @@ __device__ __forceinline__ real ld_stream(const real *p)
     return __ldg(p);
 }
 
-template <typename real>
+template <typename real, int STCS>
 __device__ __forceinline__ void st_stream(real *p, real v)
 {
-    __stcs(p, v);  // evict-first: dst is not re-read in this sweep
+    if (STCS)
+        __stcs(p, v);  // evict-first: dst is not re-read in this sweep
+    else
+        *p = v;
 }
 
 // BGK collision of the pulled values (eq:lbm with eq:feq, centred, rho0 = 1):
@@ -72,8 +75,8 @@ __device__ __forceinline__ void collide(real (&p)[Q], real omega)
 #undef LBM_PAIR
 }
 
-template <typename real>
-__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY) sweep_kernel(const SweepArgs<real> a)
+template <typename real, int MINB, int STCS>
+__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const SweepArgs<real> a)
 {
     // Locate this block's box (binary search over the tile prefix sums).
     const int64_t b = blockIdx.x;
@@ -99,45 +102,59 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY) sweep_kernel(const SweepAr
     const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
     const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
     const uint8_t k = a.kind[fbase];
-    if (k == 2) return;  // non-fluid: never updated (R13)
 
     const real *s = a.src + pbase;
     const int64_t qs = g.qs;
     real p[Q];
-    // Pull with flag-driven half-way bounce-back (R3):
-    //   neighbour x - e_i fluid  -> p_i = src_i(x - e_i)
-    //   no-slip wall             -> p_i = src_opp(i)(x)
-    //   moving wall k            -> p_i = src_opp(i)(x) + 6 w_i rho0 e_i.u_w[k]
-    uint8_t nb[Q];
+    // Pull: p_i = src_i(x - e_i).  Issued for every cell in the box
+    // without waiting for the cell's kind byte, so the kind load and the 19
+    // PDF loads are in flight together (one DRAM round trip per cell).  The
+    // ghost / shell cells these addresses may reach lie inside the patch
+    // allocation, so the speculative loads are always in bounds.
 #pragma unroll
-    for (int i = 1; i < Q; ++i) {
+    for (int i = 0; i < Q; ++i) {
         const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-        nb[i] = k ? a.flags[fbase - sh] : (uint8_t)0;
+        p[i] = ld_stream(s + i * qs - sh);
     }
-    p[0] = ld_stream(s);
+    if (k == 2) return;  // non-fluid: never updated (R13)
+    if (k == 1) {
+        // Flag-driven half-way bounce-back (R3) for cells next to a wall:
+        //   no-slip wall  -> p_i = src_opp(i)(x)
+        //   moving wall k -> p_i = src_opp(i)(x) + 6 w_i rho0 e_i.u_w[k]
 #pragma unroll
-    for (int i = 1; i < Q; ++i) {
-        const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-        const real *addr = nb[i] ? s + OPP(i) * qs : s + i * qs - sh;
-        p[i] = ld_stream(addr);
-    }
-    if (k) {
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-            if (nb[i] >= 2) p[i] += a.corr[(nb[i] - 2) * Q + i];
+        for (int i = 1; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            const uint8_t nb = a.flags[fbase - sh];
+            if (nb != 0) {
+                real v = ld_stream(s + OPP(i) * qs);
+                if (nb >= 2) v += a.corr[(nb - 2) * Q + i];
+                p[i] = v;
+            }
+        }
     }
     collide<real>(p, a.omega);
     real *d = a.dst + pbase;
 #pragma unroll
-    for (int i = 0; i < Q; ++i) st_stream(d + i * qs, p[i]);
+    for (int i = 0; i < Q; ++i) st_stream<real, STCS>(d + i * qs, p[i]);
 }
 
+// Variant v = 2 * (min blocks per SM index) + stcs; see kSweepMinBlocks.
 template <typename real>
-cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, cudaStream_t s)
+cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s)
 {
     if (total_tiles <= 0) return cudaSuccess;
     dim3 block(SWEEP_BX, SWEEP_BY, 1);
-    sweep_kernel<real><<<(unsigned)total_tiles, block, 0, s>>>(a);
+    const unsigned grid = (unsigned)total_tiles;
+    switch (variant) {
+    case 0: sweep_kernel<real, 1, 0><<<grid, block, 0, s>>>(a); break;
+    case 1: sweep_kernel<real, 1, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: sweep_kernel<real, 2, 0><<<grid, block, 0, s>>>(a); break;
+    case 3: sweep_kernel<real, 2, 1><<<grid, block, 0, s>>>(a); break;
+    case 4: sweep_kernel<real, 3, 0><<<grid, block, 0, s>>>(a); break;
+    case 5: sweep_kernel<real, 3, 1><<<grid, block, 0, s>>>(a); break;
+    case 6: sweep_kernel<real, 4, 0><<<grid, block, 0, s>>>(a); break;
+    default: sweep_kernel<real, 4, 1><<<grid, block, 0, s>>>(a); break;
+    }
     return cudaGetLastError();
 }
 
@@ -452,7 +469,7 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
 }
 
 #define LBM_INSTANTIATE(real)                                                                                   \
-    template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, cudaStream_t);                    \
+    template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, int, cudaStream_t);                    \
     template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
                                                     const real *, real *, const Geom &, cudaStream_t);          \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \

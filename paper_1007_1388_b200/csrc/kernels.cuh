@@ -26,8 +26,10 @@ struct SweepArgs {
     int nboxes;
 };
 
+// variant = 2 * m + stcs, min blocks per SM = m + 1 (m = 0..3), stcs = evict-first stores.
 template <typename real>
-cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, cudaStream_t s);
+cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s);
+constexpr int kSweepVariants = 8;
 
 template <typename real>
 cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,

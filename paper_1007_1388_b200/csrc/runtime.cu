@@ -58,6 +58,7 @@ struct TimingSlot {
     cudaEvent_t ev[kEvPerSlot];
     bool used = false;
     bool overlap = false;
+    bool exchange = false;  // exchange phases were recorded (there was exchange work)
 };
 
 }  // namespace
@@ -69,6 +70,7 @@ struct lbm_ctx {
     int esize = 8;
     int device = 0;
     int align = kAlignDefault;
+    int sweep_variant[2] = {6, 7};  // [fp32, fp64]: 4 blocks/SM (tools/sweep_tune.py); env LBM_SWEEP_VARIANT
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     bool own_stream = false;
     void *grid[2] = {nullptr, nullptr};
@@ -423,9 +425,9 @@ lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
     if (b.tiles == 0) return LBM_OK;
     cudaError_t e;
     if (ctx->esize == 8)
-        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, s);
+        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant[1], s);
     else
-        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, s);
+        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, ctx->sweep_variant[0], s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_kernel launch", __LINE__);
     ctx->launches += 1;
     return LBM_OK;
@@ -473,6 +475,9 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts)
 {
     void *grid = ctx->grid[gi];
     lbm_status st;
+    const bool work = ctx->pack_all.n > 0 || ctx->has_remote || ctx->unpack.n > 0;
+    if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
+    if (ts) ts->exchange = true;
     if (ts) CK(cudaEventRecord(ts->ev[2], s));
     if ((st = launch_copy(ctx, ctx->pack_all, grid, grid, nullptr, ctx->sendbuf, s))) return st;
     if (ts) CK(cudaEventRecord(ts->ev[3], s));
@@ -495,16 +500,18 @@ lbm_status accumulate_slot(lbm_ctx *ctx, TimingSlot &ts)
         return (double)ms;
     };
     if (!ts.overlap) {
-        ctx->phase_ms[PH_SWEEP] += el(1, 2);
-        ctx->phase_ms[PH_PACK] += el(2, 3);
-        ctx->phase_ms[PH_NCCL] += el(3, 4);
-        ctx->phase_ms[PH_UNPACK] += el(4, 5);
+        ctx->phase_ms[PH_SWEEP] += el(0, ts.exchange ? 2 : kEvPerSlot - 1);
         ctx->phase_count[PH_SWEEP] += 1;
-        ctx->phase_count[PH_PACK] += 1;
-        ctx->phase_count[PH_NCCL] += 1;
-        ctx->phase_count[PH_UNPACK] += 1;
+        if (ts.exchange) {
+            ctx->phase_ms[PH_PACK] += el(2, 3);
+            ctx->phase_ms[PH_NCCL] += el(3, 4);
+            ctx->phase_ms[PH_UNPACK] += el(4, 5);
+            ctx->phase_count[PH_PACK] += 1;
+            ctx->phase_count[PH_NCCL] += 1;
+            ctx->phase_count[PH_UNPACK] += 1;
+        }
     } else {
-        ctx->phase_ms[PH_SHELL] += el(1, 2);
+        ctx->phase_ms[PH_SHELL] += el(0, 2);
         ctx->phase_ms[PH_PACK] += el(2, 3);
         ctx->phase_ms[PH_NCCL] += el(6, 7);
         ctx->phase_ms[PH_UNPACK] += el(7, 8);
@@ -539,8 +546,8 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         if ((st = accumulate_slot(ctx, *ts))) return st;
         ts->used = true;
         ts->overlap = ctx->use_overlap;
+        ts->exchange = false;
         CK(cudaEventRecord(ts->ev[0], s));
-        CK(cudaEventRecord(ts->ev[1], s));
     }
     const int dsti = 1 - ctx->cur;
     void *dst = ctx->grid[dsti];
@@ -752,6 +759,10 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     ctx->cfg = *cfg;
     ctx->dec = dec;
     ctx->esize = cfg->precision;
+    if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {
+        int v = std::atoi(a);
+        if (v >= 0 && v < kSweepVariants) ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
+    }
     if (const char *a = std::getenv("LBM_ALIGN_BYTES")) {
         int v = std::atoi(a);
         if (v >= ctx->esize && v <= 1024 && (v & (v - 1)) == 0) ctx->align = v;

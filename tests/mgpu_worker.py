@@ -1,0 +1,78 @@
+"""Worker for tests/test_multi_gpu.py (launched by torchrun, one rank per GPU).
+
+Runs the lid-driven cavity decomposed over the ranks (NCCL ghost exchange,
+overlap on and off), gathers the owned bricks on rank 0 and checks them
+bitwise against a single-GPU run of the same lattice and against the oracle.
+Exit code 0 = pass.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    from paper_1007_1388_b200 import inputs, lbm
+    domain, patch, periodic = (48, 40, 64), (24, 20, 16), (1, 0, 0)
+    steps = 60
+    fl, wu = inputs.ldc_flags(domain, periodic)
+    fl = inputs.add_obstacles(fl, 0.03, seed=13)
+    ok = True
+    results = {}
+    for prec in (8, 4):
+        for overlap in (1, 0):
+            obj = [lbm.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, rank=rank, nranks=world,
+                            nccl_id=obj[0], periodic=periodic, overlap=overlap)
+            L.set_flags(fl, wu)
+            f0 = inputs.noise_pdfs(domain, L.owned_lo, L.owned_hi)
+            L.set_pdfs(f0)
+            L.step(steps)
+            mine = (L.owned_lo, L.owned_hi, L.get_pdfs())
+            info = L.info()
+            L.close()
+            parts = [None] * world
+            dist.all_gather_object(parts, mine)
+            if rank == 0:
+                full = np.zeros((domain[2], domain[1], domain[0], 19))
+                for lo, hi, a in parts:
+                    full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
+                results[(prec, overlap)] = full
+                print(f"prec={prec} overlap={overlap} peers={info['peers']} "
+                      f"halo={info['halo_bytes_remote_per_step']}", flush=True)
+    if rank == 0:
+        import oracle
+        ref = oracle.run(inputs.noise_pdfs(domain), fl, wu, inputs.LDC_OMEGA, steps, periodic=periodic,
+                         nthreads=oracle.max_threads())
+        mask = fl[1:-1, 1:-1, 1:-1] == 0
+        for prec in (8, 4):
+            with lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, periodic=periodic) as L:
+                L.set_flags(fl, wu)
+                L.set_pdfs(inputs.noise_pdfs(domain))
+                L.step(steps)
+                single = L.get_pdfs()
+            for overlap in (1, 0):
+                same = np.array_equal(results[(prec, overlap)], single)
+                err = float(np.abs(results[(prec, overlap)][mask] - ref[mask]).max())
+                tol = 1e-12 if prec == 8 else 1e-5
+                print(f"prec={prec} overlap={overlap} bitwise_vs_1gpu={same} max|oracle diff|={err:.3e}", flush=True)
+                ok = ok and same and err <= tol
+    flag = torch.tensor([1 if ok else 0])
+    dist.broadcast(flag, 0)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
