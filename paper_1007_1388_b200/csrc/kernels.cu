@@ -12,6 +12,7 @@
 // coalesced, sector-aligned stores.
 #include <cstdint>
 
+#include "collide.cuh"
 #include "kernels.cuh"
 
 namespace lbm {
@@ -34,45 +35,6 @@ __device__ __forceinline__ void st_stream(real *p, real v)
         __stcs(p, v);  // evict-first: dst is not re-read in this sweep
     else
         *p = v;
-}
-
-// BGK collision of the pulled values (eq:lbm with eq:feq, centred, rho0 = 1):
-//   drho = sum p_i, u = sum e_i p_i / rho0,
-//   p_i <- p_i - omega (p_i - w_i [drho + 3 e_i.u + 4.5 (e_i.u)^2 - 1.5 u.u])
-// evaluated pairwise for opposite directions (e.u changes sign, the even part
-// of f^eq is shared).
-template <typename real>
-__device__ __forceinline__ void collide(real (&p)[Q], real omega)
-{
-    const real drho = p[0] + p[1] + p[2] + p[3] + p[4] + p[5] + p[6] + p[7] + p[8] + p[9] + p[10] + p[11] +
-                      p[12] + p[13] + p[14] + p[15] + p[16] + p[17] + p[18];
-    const real ux = (p[1] - p[2]) + (p[7] - p[8]) + (p[9] - p[10]) + (p[11] - p[12]) + (p[13] - p[14]);
-    const real uy = (p[3] - p[4]) + (p[7] - p[8]) - (p[9] - p[10]) + (p[15] - p[16]) + (p[17] - p[18]);
-    const real uz = (p[5] - p[6]) + (p[11] - p[12]) - (p[13] - p[14]) + (p[15] - p[16]) - (p[17] - p[18]);
-    const real c0 = real(1) - omega;
-    const real base = drho - real(1.5) * (ux * ux + uy * uy + uz * uz);
-    const real w0 = omega * real(1.0 / 3.0);
-    const real w1 = omega * real(1.0 / 18.0);
-    const real w2 = omega * real(1.0 / 36.0);
-    p[0] = c0 * p[0] + w0 * base;
-#define LBM_PAIR(a, b, eu, w)                              \
-    {                                                      \
-        const real e_ = (eu);                              \
-        const real t_ = base + real(4.5) * e_ * e_;        \
-        const real s_ = real(3) * e_;                      \
-        p[a] = c0 * p[a] + (w) * (t_ + s_);                \
-        p[b] = c0 * p[b] + (w) * (t_ - s_);                \
-    }
-    LBM_PAIR(1, 2, ux, w1)
-    LBM_PAIR(3, 4, uy, w1)
-    LBM_PAIR(5, 6, uz, w1)
-    LBM_PAIR(7, 8, ux + uy, w2)
-    LBM_PAIR(9, 10, ux - uy, w2)
-    LBM_PAIR(11, 12, ux + uz, w2)
-    LBM_PAIR(13, 14, ux - uz, w2)
-    LBM_PAIR(15, 16, uy + uz, w2)
-    LBM_PAIR(17, 18, uy - uz, w2)
-#undef LBM_PAIR
 }
 
 template <typename real, int MINB, int STCS>
@@ -106,39 +68,46 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
     const real *s = a.src + pbase;
     const int64_t qs = g.qs;
     real p[Q];
-    // Pull: p_i = src_i(x - e_i).  Issued for every cell in the box
-    // without waiting for the cell's kind byte, so the kind load and the 19
-    // PDF loads are in flight together (one DRAM round trip per cell).  The
-    // ghost / shell cells these addresses may reach lie inside the patch
-    // allocation, so the speculative loads are always in bounds.
+    // Pull: p_i = src_i(x - e_i), branch-free.  When x - e_i is a
+    // wall cell, its slot i already holds the half-way bounce-back value
+    // f_opp(i)(x) + 6 w_i rho0 e_i.u_w (R3), written there by x's
+    // own update of the previous step (store-side bounce-back below) or by
+    // bb_fill after the state was set.  Issued for every cell in the box
+    // together with the kind byte (one DRAM round trip per cell).
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
         p[i] = ld_stream(s + i * qs - sh);
     }
     if (k == 2) return;  // non-fluid: never updated (R13)
+    uint8_t nbf[Q];
     if (k == 1) {
-        // Flag-driven half-way bounce-back (R3) for cells next to a wall:
-        //   no-slip wall  -> p_i = src_opp(i)(x)
-        //   moving wall k -> p_i = src_opp(i)(x) + 6 w_i rho0 e_i.u_w[k]
 #pragma unroll
-        for (int i = 1; i < Q; ++i) {
-            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-            const uint8_t nb = a.flags[fbase - sh];
-            if (nb != 0) {
-                real v = ld_stream(s + OPP(i) * qs);
-                if (nb >= 2) v += a.corr[(nb - 2) * Q + i];
-                p[i] = v;
-            }
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            nbf[j] = a.flags[fbase + sh];  // flag of x + e_j
         }
     }
-    collide<real>(p, a.omega);
+    collide_bgk<real>(p, a.omega);
     real *d = a.dst + pbase;
 #pragma unroll
     for (int i = 0; i < Q; ++i) st_stream<real, STCS>(d + i * qs, p[i]);
+    if (k == 1) {
+        // Store-side bounce-back: f_j(x) leaving toward the wall w = x + e_j comes
+        // back to x next step as direction opp(j); park it (plus the moving-wall
+        // term of the delivered direction opp(j)) in w's slot opp(j).
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            if (nbf[j] != 0) {
+                const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                real v = p[j];
+                if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
+                d[OPP(j) * qs + sh] = v;
+            }
+        }
+    }
 }
 
-// Variant v = 2 * (min blocks per SM index) + stcs; see kSweepMinBlocks.
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s)
 {
@@ -159,10 +128,12 @@ cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int vari
 }
 
 // ---------------------------------------------------------------- ghost exchange copies
+// Non-fluid destination cells are skipped: their PDF slots hold the store-side
+// bounce-back values written by the receiving patch itself.
 template <typename real>
 __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs, const real *grid_src,
                                                             real *grid_dst, const real *buf_src,
-                                                            real *buf_dst, const Geom g)
+                                                            real *buf_dst, const uint8_t *flags, const Geom g)
 {
     const CopySeg &sg = segs[blockIdx.y];
     const int64_t nelem = sg.nelem, cells = sg.cells;
@@ -182,18 +153,19 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs,
         else
             v = grid_src[sg.src_base + q * g.qs +
                          cell_index(g, sg.src_lo[0] + cx, sg.src_lo[1] + cy, sg.src_lo[2] + cz)];
-        if (sg.dst_is_buf)
+        if (sg.dst_is_buf) {
             buf_dst[sg.dst_base + e] = v;
-        else
-            grid_dst[sg.dst_base + q * g.qs +
-                     cell_index(g, sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz)] = v;
+        } else {
+            const int64_t ci = cell_index(g, sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz);
+            if (flags[sg.dst_flag_base + ci] == 0) grid_dst[sg.dst_base + q * g.qs + ci] = v;
+        }
     }
 }
 
 template <typename real>
 cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
-                                 real *grid_dst, const real *buf_src, real *buf_dst, const Geom &g,
-                                 cudaStream_t s)
+                                 real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
+                                 const Geom &g, cudaStream_t s)
 {
     if (nseg <= 0 || max_elems <= 0) return cudaSuccess;
     int64_t bx = (max_elems + 255) / 256;
@@ -201,7 +173,7 @@ cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elem
     for (int off = 0; off < nseg; off += 65535) {
         int n = nseg - off < 65535 ? nseg - off : 65535;
         dim3 grid((unsigned)bx, (unsigned)n, 1);
-        copy_segments_kernel<real><<<grid, 256, 0, s>>>(segs + off, grid_src, grid_dst, buf_src, buf_dst, g);
+        copy_segments_kernel<real><<<grid, 256, 0, s>>>(segs + off, grid_src, grid_dst, buf_src, buf_dst, flags, g);
     }
     return cudaGetLastError();
 }
@@ -468,10 +440,54 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- bounce-back fill
+// Writes, for the current state, the store-side bounce-back values of every
+// wall-adjacent fluid cell x into its wall neighbours: grid_opp(j)(x + e_j) =
+// grid_j(x) + corr.  Needed once after the state or the flags are set; every
+// later step maintains them inside the sweep.
+template <typename real>
+__global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr,
+                               const Geom g)
+{
+    const int lp = blockIdx.y;
+    real *gp = grid + (int64_t)lp * g.ps;
+    const uint8_t *fp = flags + (int64_t)lp * g.fs;
+    const uint8_t *kp = kind + (int64_t)lp * g.fs;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.fs; e += (int64_t)gridDim.x * blockDim.x) {
+        if (kp[e] != 1) continue;
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            const uint8_t f = fp[e + sh];
+            if (f == 0) continue;
+            real v = gp[j * g.qs + e];
+            if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
+            gp[OPP(j) * g.qs + e + sh] = v;
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
+                           const Geom &g, cudaStream_t s)
+{
+    int64_t bx = (g.fs + 255) / 256;
+    if (bx > 2048) bx = 2048;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid_dim((unsigned)bx, (unsigned)n);
+        bb_fill_kernel<real><<<grid_dim, 256, 0, s>>>(grid + (int64_t)off * g.ps, flags + (int64_t)off * g.fs,
+                                                      kind + (int64_t)off * g.fs, corr, g);
+    }
+    return cudaGetLastError();
+}
+
 #define LBM_INSTANTIATE(real)                                                                                   \
     template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, int, cudaStream_t);                    \
     template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
-                                                    const real *, real *, const Geom &, cudaStream_t);          \
+                                                    const real *, real *, const uint8_t *, const Geom &,       \
+                                                    cudaStream_t);                                             \
+    template cudaError_t launch_bb_fill<real>(real *, const uint8_t *, const uint8_t *, const real *, int,      \
+                                              const Geom &, cudaStream_t);                                     \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
                                              const int *, const Geom &, real *, cudaStream_t);                 \
     template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \

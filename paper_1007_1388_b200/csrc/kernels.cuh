@@ -1,7 +1,9 @@
 // kernels.cuh -- launch wrappers of the sm_100a kernels (kernels.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include "lbm_internal.h"
 
@@ -31,10 +33,25 @@ template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s);
 constexpr int kSweepVariants = 8;
 
+// TMA-staged persistent sweep (sweep_tma.cu); variant selects the tile shape.
+template <typename real>
+void tma_tile_shape(int variant, int *tx, int *ty);
+template <typename real>
+cudaError_t make_tma_maps(const void *grid, const uint8_t *kind, const uint8_t *flags, int nlocal, const Geom &g,
+                          int variant, CUtensorMap *pdf_map, CUtensorMap *kind_map, CUtensorMap *flag_map);
+template <typename real>
+cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &kind_map, const CUtensorMap &flag_map,
+                             const SweepArgs<real> &a, int64_t total_tiles, int num_sms, int variant, cudaStream_t s);
+
 template <typename real>
 cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
-                                 real *grid_dst, const real *buf_src, real *buf_dst, const Geom &g,
-                                 cudaStream_t s);
+                                 real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
+                                 const Geom &g, cudaStream_t s);
+
+// Store-side bounce-back values of the current state (after set_pdfs / set_flags).
+template <typename real>
+cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
+                           const Geom &g, cudaStream_t s);
 
 // Build per-patch flags (incl. ghosts, periodic wrap) from the global flag
 // array (device copy, (nz+2)(ny+2)(nx+2)), then the per-cell kind.

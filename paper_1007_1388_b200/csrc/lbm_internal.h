@@ -69,6 +69,7 @@ struct Box {
 // segment: q-list major, then cells x fastest.
 struct CopySeg {
     int64_t src_base, dst_base;
+    int64_t dst_flag_base;          // flag offset of the destination patch (grid destinations)
     int32_t src_is_buf, dst_is_buf;
     int32_t src_lo[3], dst_lo[3], size[3];
     int32_t nq;

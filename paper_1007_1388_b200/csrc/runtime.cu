@@ -70,7 +70,16 @@ struct lbm_ctx {
     int esize = 8;
     int device = 0;
     int align = kAlignDefault;
-    int sweep_variant[2] = {6, 7};  // [fp32, fp64]: 4 blocks/SM (tools/sweep_tune.py); env LBM_SWEEP_VARIANT
+    // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
+    // fp32 4 blocks/SM plain stores, fp64 3 blocks/SM evict-first stores; env LBM_SWEEP_VARIANT.
+    int sweep_variant[2] = {6, 5};
+    bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
+    int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
+    int num_sms = 148;
+    int tma_variant = 0;            // tile shape (sweep_tma.cu TmaShape); env LBM_TMA_SHAPE
+    alignas(64) CUtensorMap tm_pdf[2];
+    alignas(64) CUtensorMap tm_kind;
+    alignas(64) CUtensorMap tm_flags;
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     bool own_stream = false;
     void *grid[2] = {nullptr, nullptr};
@@ -184,7 +193,7 @@ Geom make_geom(const int n[3], int esize, int align)
     return g;
 }
 
-Box make_box(int patch, const int lo[3], const int n[3])
+Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3])
 {
     Box b;
     b.patch = patch;
@@ -192,8 +201,8 @@ Box make_box(int patch, const int lo[3], const int n[3])
         b.lo[a] = lo[a];
         b.n[a] = n[a];
     }
-    b.tiles_x = (n[0] + SWEEP_BX - 1) / SWEEP_BX;
-    b.tiles_y = (n[1] + SWEEP_BY - 1) / SWEEP_BY;
+    b.tiles_x = (n[0] + ctx->tile_x - 1) / ctx->tile_x;
+    b.tiles_y = (n[1] + ctx->tile_y - 1) / ctx->tile_y;
     return b;
 }
 
@@ -258,6 +267,7 @@ CopySeg grid_to_x(const lbm_ctx *ctx, const Seg &s, bool to_buffer, int64_t buf_
         const int lrecv = ctx->dec.global_to_local(s.recv_patch);
         c.dst_is_buf = 0;
         c.dst_base = (int64_t)lrecv * ctx->g.ps;
+        c.dst_flag_base = (int64_t)lrecv * ctx->g.fs;
     }
     return c;
 }
@@ -271,6 +281,7 @@ CopySeg buffer_to_grid(const lbm_ctx *ctx, const Seg &s, int64_t buf_base)
     c.src_base = buf_base + s.offset;
     c.dst_is_buf = 0;
     c.dst_base = (int64_t)lrecv * ctx->g.ps;
+    c.dst_flag_base = (int64_t)lrecv * ctx->g.fs;
     for (int a = 0; a < 3; ++a) {
         c.dst_lo[a] = s.recv_lo[a];
         c.size[a] = s.size[a];
@@ -361,16 +372,16 @@ lbm_status setup_exchange(lbm_ctx *ctx)
         }
     }
     for (int l = 0; l < ctx->dec.nlocal; ++l) {
-        all.push_back(make_box(l, zero, n));
+        all.push_back(make_box(ctx, l, zero, n));
         bool any = false;
         for (int k = 0; k < 6; ++k) any = any || side[6 * l + k];
         if (!any) {
-            interior.push_back(make_box(l, zero, n));
+            interior.push_back(make_box(ctx, l, zero, n));
             continue;
         }
         int th[6];
         for (int a = 0; a < 3; ++a) {
-            const int t = a == 0 ? SWEEP_BX : 1;
+            const int t = a == 0 ? ctx->tile_x : 1;
             th[2 * a] = side[6 * l + 2 * a] ? std::min(t, n[a]) : 0;
             th[2 * a + 1] = side[6 * l + 2 * a + 1] ? std::min(t, n[a] - th[2 * a]) : 0;
         }
@@ -379,11 +390,16 @@ lbm_status setup_exchange(lbm_ctx *ctx)
             lo[a] = th[2 * a];
             hi[a] = n[a] - th[2 * a + 1];
         }
+        // Every tile must start on a 16-cell boundary in x (16-B aligned TMA
+        // starts for the PDF, kind and flag maps, see sweep_tma.cu): round the
+        // high-x shell start down.
+        const int xa = 16;
+        hi[0] = std::max(lo[0], hi[0] / xa * xa);
         // z slabs (full xy), then y slabs (full x, inner z), then x slabs (inner y, z)
         auto add = [&](int x0, int x1, int y0, int y1, int z0, int z1) {
             if (x1 <= x0 || y1 <= y0 || z1 <= z0) return;
             int blo[3] = {x0, y0, z0}, bn[3] = {x1 - x0, y1 - y0, z1 - z0};
-            shell.push_back(make_box(l, blo, bn));
+            shell.push_back(make_box(ctx, l, blo, bn));
         };
         add(0, n[0], 0, n[1], 0, lo[2]);
         add(0, n[0], 0, n[1], hi[2], n[2]);
@@ -393,7 +409,7 @@ lbm_status setup_exchange(lbm_ctx *ctx)
         add(hi[0], n[0], lo[1], hi[1], lo[2], hi[2]);
         if (hi[0] > lo[0] && hi[1] > lo[1] && hi[2] > lo[2]) {
             int bn[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
-            interior.push_back(make_box(l, lo, bn));
+            interior.push_back(make_box(ctx, l, lo, bn));
         }
     }
     if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
@@ -424,7 +440,15 @@ lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
 {
     if (b.tiles == 0) return LBM_OK;
     cudaError_t e;
-    if (ctx->esize == 8)
+    if (ctx->use_tma) {
+        const CUtensorMap &pm = ctx->tm_pdf[ctx->cur];
+        if (ctx->esize == 8)
+            e = launch_sweep_tma<double>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
+                                         ctx->num_sms, ctx->tma_variant, s);
+        else
+            e = launch_sweep_tma<float>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<float>(ctx, b), b.tiles,
+                                        ctx->num_sms, ctx->tma_variant, s);
+    } else if (ctx->esize == 8)
         e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant[1], s);
     else
         e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, ctx->sweep_variant[0], s);
@@ -440,10 +464,10 @@ lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *gri
     cudaError_t e;
     if (ctx->esize == 8)
         e = launch_copy_segments<double>(d.segs, d.n, d.max_elems, (const double *)grid_src, (double *)grid_dst,
-                                         (const double *)buf_src, (double *)buf_dst, ctx->g, s);
+                                         (const double *)buf_src, (double *)buf_dst, ctx->flags, ctx->g, s);
     else
         e = launch_copy_segments<float>(d.segs, d.n, d.max_elems, (const float *)grid_src, (float *)grid_dst,
-                                        (const float *)buf_src, (float *)buf_dst, ctx->g, s);
+                                        (const float *)buf_src, (float *)buf_dst, ctx->flags, ctx->g, s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "copy_segments launch", __LINE__);
     ctx->launches += (d.n + 65534) / 65535;
     return LBM_OK;
@@ -487,6 +511,23 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts)
     if (ts) CK(cudaEventRecord(ts->ev[4], s));
     if ((st = launch_copy(ctx, ctx->unpack, nullptr, grid, ctx->recvbuf, nullptr, s))) return st;
     if (ts) CK(cudaEventRecord(ts->ev[5], s));
+    return LBM_OK;
+}
+
+// After the state or the flags change: refresh the ghost layers of the current
+// grid and park the store-side bounce-back values in the wall cells.
+lbm_status refresh_state(lbm_ctx *ctx)
+{
+    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr);
+    if (st) return st;
+    cudaError_t e = ctx->esize == 8
+                        ? launch_bb_fill<double>((double *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
+                                                 (const double *)ctx->corr, ctx->dec.nlocal, ctx->g, ctx->stream)
+                        : launch_bb_fill<float>((float *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
+                                                (const float *)ctx->corr, ctx->dec.nlocal, ctx->g, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "bb_fill", __LINE__);
+    ctx->launches += (ctx->dec.nlocal + 65534) / 65535;
+    CK(cudaStreamSynchronize(ctx->stream));
     return LBM_OK;
 }
 
@@ -763,6 +804,20 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         int v = std::atoi(a);
         if (v >= 0 && v < kSweepVariants) ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
     }
+    if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
+        if (std::string(a) == "simt") ctx->use_tma = false;
+        if (std::string(a) == "tma") ctx->use_tma = true;
+    }
+    if (const char *a = std::getenv("LBM_TMA_SHAPE")) {
+        int v = std::atoi(a);
+        if (v >= 0 && v <= 2) ctx->tma_variant = v;
+    }
+    if (ctx->use_tma) {
+        if (ctx->esize == 8)
+            tma_tile_shape<double>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
+        else
+            tma_tile_shape<float>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
+    }
     if (const char *a = std::getenv("LBM_ALIGN_BYTES")) {
         int v = std::atoi(a);
         if (v >= ctx->esize && v <= 1024 && (v & (v - 1)) == 0) ctx->align = v;
@@ -811,9 +866,15 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         }
         ctx->own_stream = true;
     }
-    if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess) {
-        ctx->err = "cudaStreamCreate failed";
-        return bail(LBM_ERR_CUDA);
+    {
+        // The exchange stream gets the highest priority so the NCCL / unpack
+        // blocks are scheduled ahead of the interior sweep they overlap with.
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        if (cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate failed";
+            return bail(LBM_ERR_CUDA);
+        }
     }
     for (auto &sl : ctx->slots)
         for (auto &ev : sl.ev)
@@ -853,6 +914,24 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if (cudaMemcpy(ctx->d_origin, origin.data(), origin.size() * sizeof(int), cudaMemcpyHostToDevice) !=
             cudaSuccess)
             return bail(LBM_ERR_CUDA);
+    }
+    {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            ctx->num_sms = sms;
+    }
+    if (ctx->use_tma) {
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = ctx->esize == 8
+                                ? make_tma_maps<double>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
+                                                        ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags)
+                                : make_tma_maps<float>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
+                                                       ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags);
+            if (e != cudaSuccess) {
+                ctx->err = "cuTensorMapEncodeTiled failed for the PDF / kind arrays";
+                return bail(LBM_ERR_CUDA);
+            }
+        }
     }
     if ((st = setup_exchange(ctx))) return bail(st);
     // NCCL communicator (bootstrap id broadcast by the caller, e.g. torch.distributed)
@@ -996,7 +1075,9 @@ LBM_API lbm_status lbm_set_flags(lbm_ctx *ctx, const uint8_t *flags, const doubl
     const char *m = validate_flags(ctx->dec, flags, wall_u, nvel);
     if (m[0]) return ctx->fail(LBM_ERR_ARG, m);
     CK(cudaStreamSynchronize(ctx->stream));
-    return apply_flags(ctx, flags, wall_u, nvel);
+    lbm_status st = apply_flags(ctx, flags, wall_u, nvel);
+    if (st) return st;
+    return refresh_state(ctx);
 }
 
 LBM_API lbm_status lbm_get_flags(lbm_ctx *ctx, uint8_t *out)
@@ -1033,9 +1114,7 @@ LBM_API lbm_status lbm_set_pdfs(lbm_ctx *ctx, const double *f)
     CK(cudaStreamSynchronize(ctx->stream));
     lbm_status st = transfer_chunks(ctx, const_cast<double *>(f), true, 0, nullptr, nullptr);
     if (st) return st;
-    if ((st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr))) return st;
-    CK(cudaStreamSynchronize(ctx->stream));
-    return LBM_OK;
+    return refresh_state(ctx);
 }
 
 LBM_API lbm_status lbm_init_noise(lbm_ctx *ctx, uint64_t seed)
@@ -1050,10 +1129,7 @@ LBM_API lbm_status lbm_init_noise(lbm_ctx *ctx, uint64_t seed)
                                               ctx->g, ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "noise_kernel", __LINE__);
     ctx->launches += 1;
-    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr);
-    if (st) return st;
-    CK(cudaStreamSynchronize(ctx->stream));
-    return LBM_OK;
+    return refresh_state(ctx);
 }
 
 LBM_API lbm_status lbm_step_async(lbm_ctx *ctx, int64_t nsteps)

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--variants", default="0-7")
     ap.add_argument("--aligns", default="128")
     ap.add_argument("--precisions", default="8,4")
+    ap.add_argument("--impls", default="tma,simt")
+    ap.add_argument("--shapes", default="0-2")
     args = ap.parse_args()
     import torch
     from paper_1007_1388_b200 import inputs, lbm
@@ -40,10 +42,16 @@ def main():
     patch = (args.patch,) * 3 if args.patch else n
     fl, wu = inputs.ldc_flags(n)
     results = []
+    combos = []
+    for impl in args.impls.split(","):
+        for v in (parse_list(args.variants) if impl == "simt" else parse_list(args.shapes)):
+            combos.append((impl, v))
     for prec in parse_list(args.precisions):
         for align in parse_list(args.aligns):
-            for v in parse_list(args.variants):
-                os.environ["LBM_SWEEP_VARIANT"] = str(v)
+            for impl, v in combos:
+                os.environ["LBM_SWEEP_IMPL"] = impl
+                os.environ["LBM_SWEEP_VARIANT"] = str(v) if impl == "simt" else "7"
+                os.environ["LBM_TMA_SHAPE"] = str(v) if impl == "tma" else "0"
                 os.environ["LBM_ALIGN_BYTES"] = str(align)
                 L = lbm.Lattice(n, patch, inputs.LDC_OMEGA, prec, device=0)
                 L.set_flags(fl, wu)
@@ -61,7 +69,7 @@ def main():
                 L.close()
                 mfl = fluid / (ms / 1e3) / 1e6
                 gbs = mfl * 1e6 * 2 * 19 * prec / 1e9
-                r = dict(prec=prec, variant=v, align=align, ms=ms, mflups=mfl, alg_gbs=gbs)
+                r = dict(prec=prec, impl=impl, variant=v, align=align, ms=ms, mflups=mfl, alg_gbs=gbs)
                 results.append(r)
                 print(json.dumps(r), flush=True)
     best = {}
