@@ -37,7 +37,7 @@ __device__ __forceinline__ void st_stream(real *p, real v)
         *p = v;
 }
 
-template <typename real, int MINB, int STCS>
+template <typename real, int MINB, int STCS, int ZC>
 __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const SweepArgs<real> a)
 {
     // Locate this block's box (binary search over the tile prefix sums).
@@ -48,26 +48,28 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
         if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
     }
     const Box &bx = a.boxes[lo];
-    int64_t t = b - a.tile_prefix[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
     const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
-    const int tx = (int)(t % tiles_x);
+    const int tx = t % tiles_x;
     t /= tiles_x;
-    const int ty = (int)(t % tiles_y);
-    const int tz = (int)(t / tiles_y);
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
     const int x = bx.lo[0] + tx * SWEEP_BX + (int)threadIdx.x;
     const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
-    const int z = bx.lo[2] + tz;
+    const int z0 = bx.lo[2] + tz * ZC;
     if (x >= bx.lo[0] + bx.n[0] || y >= bx.lo[1] + bx.n[1]) return;
+    const int zend = bx.lo[2] + bx.n[2];
 
     const Geom &g = a.g;
-    const int64_t cell = cell_index(g, x, y, z);
-    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
-    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
-    const uint8_t k = a.kind[fbase];
-
-    const real *s = a.src + pbase;
     const int64_t qs = g.qs;
-    real p[Q];
+    const int64_t cell0 = cell_index(g, x, y, z0);
+    const int64_t pbase0 = (int64_t)bx.patch * g.ps + cell0;
+    const int64_t fbase0 = (int64_t)bx.patch * g.fs + cell0;
+    // ZC cells per thread along z (ZC = 2 doubles the independent loads in flight).
+    uint8_t k[ZC];
+    real p[ZC][Q];
+#pragma unroll
+    for (int c = 0; c < ZC; ++c) k[c] = (z0 + c < zend) ? a.kind[fbase0 + c * g.plane] : (uint8_t)2;
     // Pull: p_i = src_i(x - e_i), branch-free.  When x - e_i is a
     // wall cell, its slot i already holds the half-way bounce-back value
     // f_opp(i)(x) + 6 w_i rho0 e_i.u_w (R3), written there by x's
@@ -75,39 +77,50 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
     // bb_fill after the state was set.  Issued for every cell in the box
     // together with the kind byte (one DRAM round trip per cell).
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-        p[i] = ld_stream(s + i * qs - sh);
-    }
-    if (k == 2) return;  // non-fluid: never updated (R13)
-    uint8_t nbf[Q];
-    if (k == 1) {
+    for (int c = 0; c < ZC; ++c) {
+        if (c > 0 && z0 + c >= zend) break;
+        const real *s = a.src + pbase0 + c * g.plane;
 #pragma unroll
-        for (int j = 1; j < Q; ++j) {
-            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-            nbf[j] = a.flags[fbase + sh];  // flag of x + e_j
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            p[c][i] = ld_stream(s + i * qs - sh);
         }
     }
-    collide_bgk<real>(p, a.omega);
-    real *d = a.dst + pbase;
 #pragma unroll
-    for (int i = 0; i < Q; ++i) st_stream<real, STCS>(d + i * qs, p[i]);
-    if (k == 1) {
-        // Store-side bounce-back: f_j(x) leaving toward the wall w = x + e_j comes
-        // back to x next step as direction opp(j); park it (plus the moving-wall
-        // term of the delivered direction opp(j)) in w's slot opp(j).
+    for (int c = 0; c < ZC; ++c) {
+        if (k[c] == 2) continue;  // non-fluid (or beyond the box): never updated (R13)
+        const int64_t fbase = fbase0 + c * g.plane;
+        uint8_t nbf[Q];
+        if (k[c] == 1) {
 #pragma unroll
-        for (int j = 1; j < Q; ++j) {
-            if (nbf[j] != 0) {
+            for (int j = 1; j < Q; ++j) {
                 const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-                real v = p[j];
-                if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
-                d[OPP(j) * qs + sh] = v;
+                nbf[j] = a.flags[fbase + sh];  // flag of x + e_j
+            }
+        }
+        collide_bgk<real>(p[c], a.omega);
+        real *d = a.dst + pbase0 + c * g.plane;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) st_stream<real, STCS>(d + i * qs, p[c][i]);
+        if (k[c] == 1) {
+            // Store-side bounce-back: f_j(x) leaving toward the wall w = x + e_j comes
+            // back to x next step as direction opp(j); park it (plus the moving-wall
+            // term of the delivered direction opp(j)) in w's slot opp(j).
+#pragma unroll
+            for (int j = 1; j < Q; ++j) {
+                if (nbf[j] != 0) {
+                    const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                    real v = p[c][j];
+                    if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
+                    d[OPP(j) * qs + sh] = v;
+                }
             }
         }
     }
 }
 
+// variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first
+// stores, one cell per thread; 8..11: two cells per thread along z.
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s)
 {
@@ -115,14 +128,18 @@ cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int vari
     dim3 block(SWEEP_BX, SWEEP_BY, 1);
     const unsigned grid = (unsigned)total_tiles;
     switch (variant) {
-    case 0: sweep_kernel<real, 1, 0><<<grid, block, 0, s>>>(a); break;
-    case 1: sweep_kernel<real, 1, 1><<<grid, block, 0, s>>>(a); break;
-    case 2: sweep_kernel<real, 2, 0><<<grid, block, 0, s>>>(a); break;
-    case 3: sweep_kernel<real, 2, 1><<<grid, block, 0, s>>>(a); break;
-    case 4: sweep_kernel<real, 3, 0><<<grid, block, 0, s>>>(a); break;
-    case 5: sweep_kernel<real, 3, 1><<<grid, block, 0, s>>>(a); break;
-    case 6: sweep_kernel<real, 4, 0><<<grid, block, 0, s>>>(a); break;
-    default: sweep_kernel<real, 4, 1><<<grid, block, 0, s>>>(a); break;
+    case 0: sweep_kernel<real, 1, 0, 1><<<grid, block, 0, s>>>(a); break;
+    case 1: sweep_kernel<real, 1, 1, 1><<<grid, block, 0, s>>>(a); break;
+    case 2: sweep_kernel<real, 2, 0, 1><<<grid, block, 0, s>>>(a); break;
+    case 3: sweep_kernel<real, 2, 1, 1><<<grid, block, 0, s>>>(a); break;
+    case 4: sweep_kernel<real, 3, 0, 1><<<grid, block, 0, s>>>(a); break;
+    case 5: sweep_kernel<real, 3, 1, 1><<<grid, block, 0, s>>>(a); break;
+    case 6: sweep_kernel<real, 4, 0, 1><<<grid, block, 0, s>>>(a); break;
+    case 7: sweep_kernel<real, 4, 1, 1><<<grid, block, 0, s>>>(a); break;
+    case 8: sweep_kernel<real, 2, 0, 2><<<grid, block, 0, s>>>(a); break;
+    case 9: sweep_kernel<real, 2, 1, 2><<<grid, block, 0, s>>>(a); break;
+    case 10: sweep_kernel<real, 3, 0, 2><<<grid, block, 0, s>>>(a); break;
+    default: sweep_kernel<real, 3, 1, 2><<<grid, block, 0, s>>>(a); break;
     }
     return cudaGetLastError();
 }

@@ -28,10 +28,13 @@ struct SweepArgs {
     int nboxes;
 };
 
-// variant = 2 * m + stcs, min blocks per SM = m + 1 (m = 0..3), stcs = evict-first stores.
+// variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first stores,
+// one cell per thread; variants 8..11: two cells per thread along z (tiles span
+// 2 planes), min blocks 2 / 3, stcs 0 / 1.
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s);
-constexpr int kSweepVariants = 8;
+constexpr int kSweepVariants = 12;
+__host__ __device__ constexpr int sweep_cells_z(int variant) { return variant >= 8 ? 2 : 1; }
 
 // TMA-staged persistent sweep (sweep_tma.cu); variant selects the tile shape.
 template <typename real>

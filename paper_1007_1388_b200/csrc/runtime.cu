@@ -211,7 +211,10 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
     std::vector<int64_t> prefix(boxes.size() + 1, 0);
     for (size_t i = 0; i < boxes.size(); ++i) {
         const Box &b = boxes[i];
-        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0) ? (int64_t)b.tiles_x * b.tiles_y * b.n[2] : 0;
+        const int zc = ctx->use_tma ? 1 : sweep_cells_z(ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]);
+        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0)
+                        ? (int64_t)b.tiles_x * b.tiles_y * ((b.n[2] + zc - 1) / zc)
+                        : 0;
         prefix[i + 1] = prefix[i] + t;
     }
     out.n = (int)boxes.size();
