@@ -207,6 +207,7 @@ def main():
     ap.add_argument("--impl", choices=("product", "reference"), default="product")
     ap.add_argument("--overlap", type=int, default=1)
     ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--layout", choices=("ab", "aa"), default="ab")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -247,7 +248,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, rank=rank, nranks=world,
-                    proc_grid=pgrid, nccl_id=nccl_id, overlap=args.overlap, use_graphs=args.graphs)
+                    proc_grid=pgrid, nccl_id=nccl_id, overlap=args.overlap, use_graphs=args.graphs,
+                    layout=lbm.LBM_LAYOUT_AA if args.layout == "aa" else lbm.LBM_LAYOUT_AB)
     fl, wu = inputs.ldc_flags(domain)
     L.set_flags(fl, wu)
     del fl
@@ -367,7 +369,7 @@ def main():
                        "proc_grid": list(pgrid), "parallelism": f"block-decomposition x{world}",
                        "fluid_cells": fluid_global, "mflups_per_gpu": value / world,
                        "omega": inputs.LDC_OMEGA, "lid_u": inputs.LDC_U, "init": "dyadic noise seed 1388",
-                       "overlap": bool(args.overlap), "graphs": bool(args.graphs),
+                       "overlap": bool(args.overlap), "graphs": bool(args.graphs), "layout": args.layout,
                        "l2": f"no flush: PDF state {2 * 19 * esize * fluid_local / 1e9:.2f} GB/GPU >> 126 MB L2",
                        "halo_bytes_remote_per_step": info["halo_bytes_remote_per_step"],
                        "row_pitch_elems": info["row_pitch_elems"], "align_bytes": info["align_bytes"]},

@@ -82,6 +82,14 @@ typedef enum { LBM_FP32 = 4, LBM_FP64 = 8 } lbm_precision; /* storage AND arithm
  * 2 + k: wall moving with velocity wall_u[k] (k < nvel <= 254).              */
 enum { LBM_FLUID = 0, LBM_NOSLIP = 1, LBM_VELOCITY0 = 2 };
 
+/* PDF storage layout (north_star (a)).                   */
+enum {
+    LBM_LAYOUT_AB = 0, /* two PDF grids, pull from src, write dst, swap        */
+    LBM_LAYOUT_AA = 1  /* one PDF grid, AA pattern: alternating in-place PULL / LOCAL
+                          steps, half the memory; results equal LBM_LAYOUT_AB bitwise
+                          after every even step count                               */
+};
+
 /* Exchange transport for neighbouring patches.                               */
 enum {
     LBM_EXCHANGE_AUTO = 0,        /* same GPU: direct ghost copy; other GPU: NCCL      */
@@ -107,6 +115,7 @@ typedef struct {
                                the interiors are swept (multi-GPU); 0 = sequential              */
     int32_t use_graphs;     /* 1 = capture the step pair in a CUDA graph and replay it          */
     void *stream;           /* cudaStream_t for all compute launches; NULL = library-owned      */
+    int32_t layout;         /* LBM_LAYOUT_AB or LBM_LAYOUT_AA                                    */
 } lbm_config;
 
 /* Per-ctx information (lbm_get_info).                                         */
@@ -135,6 +144,8 @@ typedef struct {
     int64_t row_pitch_elems;               /* x pitch of a patch row (padding / alignment)  */
     int32_t align_bytes;                   /* alignment of interior x = 0                   */
     int32_t graphs_active;
+    int32_t layout;                        /* LBM_LAYOUT_*                                  */
+    int32_t aa_phase;                      /* AA: 0 swapped (even step count), 1 streamed   */
 } lbm_info;
 
 /* One remote message of the static exchange plan (lbm_plan, host-only).      */
@@ -170,6 +181,8 @@ LBM_API lbm_status lbm_create_ex(const lbm_config *cfg, lbm_ctx **out);
 LBM_API lbm_status lbm_destroy(lbm_ctx *ctx);
 
 /* Cell flags for the WHOLE global lattice incl. its one-cell shell:
+ * (LBM_LAYOUT_AA: only valid after an even number of steps since the last
+ * set_pdfs / init_noise, else LBM_ERR_STATE.)
  * uint8 [(nz+2)][(ny+2)][(nx+2)], x fastest (every rank passes the same
  * array).  wall_u: nvel x 3 doubles, velocity of flag 2 + k (may be NULL when
  * nvel == 0).  Shell cells on non-periodic axes must be non-fluid, and every

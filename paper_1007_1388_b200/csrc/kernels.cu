@@ -121,6 +121,127 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
 
 // variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first
 // stores, one cell per thread; 8..11: two cells per thread along z.
+// ------------------------------------------------------------------ AA pattern
+// One PDF array, two alternating in-place kernels (north_star (a)).
+// With S_i(x) the post-collision state of the two-grid scheme:
+//   swapped  representation (after an even step count): A[x][opp(i)] = S_i(x)
+//   streamed representation (after an odd step count):  A[x][i] = p_i(x), the
+//                                                        value x pulls next
+// PULL  (swapped -> streamed): p_i = A[x - e_i][opp(i)]; collide; write out_i to
+//       A[x + e_i][i], or -- x + e_i a wall -- its bounce-back
+//       out_i + 6 w rho0 e_opp(i).u_w to A[x][opp(i)] (R3).
+// LOCAL (streamed -> swapped): p_i = A[x][i]; collide; A[x][opp(i)] = out_i, and
+//       for walls w = x + e_j the store-side bounce-back A[w][j] = out_j + corr,
+//       which the next PULL gathers branch-free.
+// Every slot has exactly one writer per step and is read only by it, so both
+// kernels run in place without races; the results equal the two-grid scheme
+// bitwise after every even step count.
+template <typename real, bool PULL, int MINB, int STCS>
+__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(const SweepArgs<real> a)
+{
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    const int x = bx.lo[0] + tx * SWEEP_BX + (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    if (x >= bx.lo[0] + bx.n[0] || y >= bx.lo[1] + bx.n[1]) return;
+
+    const Geom &g = a.g;
+    const int64_t qs = g.qs;
+    const int64_t cell = cell_index(g, x, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k = a.kind[fbase];
+    real *A = a.dst + pbase;  // in place: src == dst
+    real p[Q];
+    if (PULL) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            p[i] = ld_stream((const real *)A + OPP(i) * qs - sh);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) p[i] = ld_stream((const real *)A + i * qs);
+    }
+    if (k == 2) return;
+    uint8_t nbf[Q];
+    if (k == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            nbf[j] = a.flags[fbase + sh];  // flag of x + e_j
+        }
+    }
+    collide_bgk<real>(p, a.omega);
+    if (PULL) {
+        st_stream<real, STCS>(A, p[0]);
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            if (k == 1 && nbf[i] != 0) {
+                real v = p[i];
+                if (nbf[i] >= 2) v += a.corr[(nbf[i] - 2) * Q + OPP(i)];
+                A[OPP(i) * qs] = v;
+            } else {
+                st_stream<real, STCS>(A + i * qs + sh, p[i]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) st_stream<real, STCS>(A + OPP(i) * qs, p[i]);
+        if (k == 1) {
+#pragma unroll
+            for (int j = 1; j < Q; ++j) {
+                if (nbf[j] != 0) {
+                    const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                    real v = p[j];
+                    if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
+                    A[j * qs + sh] = v;
+                }
+            }
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s)
+{
+    if (total_tiles <= 0) return cudaSuccess;
+    dim3 block(SWEEP_BX, SWEEP_BY, 1);
+    const unsigned grid = (unsigned)total_tiles;
+    const int v = variant & 7;  // min blocks / store hint as for the two-grid sweep
+    if (pull) {
+        switch (v) {
+        case 4: sweep_aa_kernel<real, true, 3, 0><<<grid, block, 0, s>>>(a); break;
+        case 5: sweep_aa_kernel<real, true, 3, 1><<<grid, block, 0, s>>>(a); break;
+        case 6: sweep_aa_kernel<real, true, 4, 0><<<grid, block, 0, s>>>(a); break;
+        case 7: sweep_aa_kernel<real, true, 4, 1><<<grid, block, 0, s>>>(a); break;
+        default: sweep_aa_kernel<real, true, 2, 0><<<grid, block, 0, s>>>(a); break;
+        }
+    } else {
+        switch (v) {
+        case 4: sweep_aa_kernel<real, false, 3, 0><<<grid, block, 0, s>>>(a); break;
+        case 5: sweep_aa_kernel<real, false, 3, 1><<<grid, block, 0, s>>>(a); break;
+        case 6: sweep_aa_kernel<real, false, 4, 0><<<grid, block, 0, s>>>(a); break;
+        case 7: sweep_aa_kernel<real, false, 4, 1><<<grid, block, 0, s>>>(a); break;
+        default: sweep_aa_kernel<real, false, 2, 0><<<grid, block, 0, s>>>(a); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s)
 {
@@ -173,8 +294,19 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs,
         if (sg.dst_is_buf) {
             buf_dst[sg.dst_base + e] = v;
         } else {
-            const int64_t ci = cell_index(g, sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz);
-            if (flags[sg.dst_flag_base + ci] == 0) grid_dst[sg.dst_base + q * g.qs + ci] = v;
+            const int y[3] = {sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz};
+            const int64_t ci = cell_index(g, y[0], y[1], y[2]);
+            bool ok = flags[sg.dst_flag_base + ci] == 0;
+            if (sg.mask == 2 && ok) {
+                // AA half-exchange 2: the value was scattered by the sender's cell
+                // w = y - e_q; only entries whose writer is a fluid cell of the
+                // sender (not another patch's ghost) are delivered.
+                const int w[3] = {y[0] - EX(q), y[1] - EY(q), y[2] - EZ(q)};
+                for (int a2 = 0; a2 < 3; ++a2)
+                    if (sg.d[a2] == 0 && (w[a2] < 0 || w[a2] >= g.n[a2])) ok = false;
+                if (ok) ok = flags[sg.dst_flag_base + cell_index(g, w[0], w[1], w[2])] == 0;
+            }
+            if (ok) grid_dst[sg.dst_base + q * g.qs + ci] = v;
         }
     }
 }
@@ -291,9 +423,27 @@ __device__ __forceinline__ void owned_to_patch(const Geom &g, const int brick[3]
     lp = (bz * brick[1] + by) * brick[0] + bx;
 }
 
+// rep: 0 = two-grid (slot i holds f_i), 1 = AA swapped (slot opp(i) holds f_i),
+//      2 = AA streamed (export only: f_i(x) = A[x + e_i][i], or at a wall
+//          x + e_i the bounced value A[x][opp(i)] minus its wall term).
+__device__ __forceinline__ int rep_slot(int rep, int i) { return rep == 1 ? OPP(i) : i; }
+
+template <typename real>
+__device__ __forceinline__ double read_state(const real *gp, const uint8_t *fp, const real *corr, const Geom &g,
+                                             int rep, int i)
+{
+    if (rep != 2) return (double)gp[rep_slot(rep, i) * g.qs];
+    const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+    const uint8_t f = fp[sh];
+    if (i == 0 || f == 0) return (double)gp[i * g.qs + sh];
+    real v = gp[OPP(i) * g.qs];
+    if (f >= 2) v -= corr[(f - 2) * Q + OPP(i)];
+    return (double)v;
+}
+
 template <typename real>
 __global__ void import_kernel(const double *canon, int64_t z0, int64_t ncells, int64_t nx, int64_t ny,
-                              int b0, int b1, int b2, const Geom g, real *grid)
+                              int b0, int b1, int b2, const Geom g, real *grid, const int rep)
 {
     const int brick[3] = {b0, b1, b2};
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
@@ -306,14 +456,14 @@ __global__ void import_kernel(const double *canon, int64_t z0, int64_t ncells, i
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
         real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) gp[q * g.qs] = (real)canon[c * Q + q];
+        for (int q = 0; q < Q; ++q) gp[rep_slot(rep, q) * g.qs] = (real)canon[c * Q + q];
     }
 }
 
 template <typename real>
 __global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0, int64_t ncells, int64_t nx,
                               int64_t ny, int b0, int b1, int b2, const Geom g, int mode, double *canon,
-                              double *rho, double *u)
+                              double *rho, double *u, const int rep, const real *corr)
 {
     const int brick[3] = {b0, b1, b2};
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
@@ -325,17 +475,18 @@ __global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
         const int64_t ci = cell_index(g, lx, ly, lz);
-        const bool fluid = flags[(int64_t)lp * g.fs + ci] == 0;
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const bool fluid = fp[0] == 0;
         const real *gp = grid + (int64_t)lp * g.ps + ci;
         if (mode == 0) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? (double)gp[q * g.qs] : 0.0;
+            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
         } else {
             // Macroscopic export: rho = rho0 + sum f~, u = sum e f~ / rho0.
             double s = 0, jx = 0, jy = 0, jz = 0;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                const double v = (double)gp[q * g.qs];
+                const double v = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
                 s += v;
                 jx += EX(q) * v;
                 jy += EY(q) * v;
@@ -353,7 +504,7 @@ __global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0
 
 template <typename real>
 cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, const int64_t owned_lo[3],
-                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid,
+                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid, int rep,
                           cudaStream_t s)
 {
     (void)owned_lo;
@@ -362,14 +513,15 @@ cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, con
     int64_t nb = (ncells + 255) / 256;
     if (nb > 8192) nb = 8192;
     import_kernel<real><<<(unsigned)nb, 256, 0, s>>>(canon, z0, ncells, owned_n[0], owned_n[1], brick[0],
-                                                    brick[1], brick[2], g, grid);
+                                                    brick[1], brick[2], g, grid, rep);
     return cudaGetLastError();
 }
 
 template <typename real>
 cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, int64_t nz_chunk,
                           const int64_t owned_lo[3], const int64_t owned_n[3], const int brick[3],
-                          const Geom &g, double *canon, int mode, double *rho, double *u, cudaStream_t s)
+                          const Geom &g, double *canon, int mode, double *rho, double *u, int rep,
+                          const real *corr, cudaStream_t s)
 {
     (void)owned_lo;
     const int64_t ncells = owned_n[0] * owned_n[1] * nz_chunk;
@@ -377,7 +529,7 @@ cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, in
     int64_t nb = (ncells + 255) / 256;
     if (nb > 8192) nb = 8192;
     export_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, flags, z0, ncells, owned_n[0], owned_n[1], brick[0],
-                                                    brick[1], brick[2], g, mode, canon, rho, u);
+                                                    brick[1], brick[2], g, mode, canon, rho, u, rep, corr);
     return cudaGetLastError();
 }
 
@@ -396,7 +548,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x)
 template <typename real>
 __global__ void noise_kernel(real *grid, uint64_t seed, int64_t NX, int64_t NY, int64_t lox, int64_t loy,
                              int64_t loz, int64_t nx, int64_t ny, int64_t ncells, int b0, int b1, int b2,
-                             const Geom g)
+                             const Geom g, const int rep)
 {
     const int brick[3] = {b0, b1, b2};
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
@@ -413,47 +565,49 @@ __global__ void noise_kernel(real *grid, uint64_t seed, int64_t NX, int64_t NY, 
         for (int q = 0; q < Q; ++q) {
             const uint64_t key = gi * 19ull + (uint64_t)q + seed * 0x9E3779B97F4A7C15ull;
             const int64_t k = (int64_t)(splitmix64(key) % 2049ull) - 1024;
-            gp[q * g.qs] = (real)((double)k * (1.0 / 1048576.0));
+            gp[rep_slot(rep, q) * g.qs] = (real)((double)k * (1.0 / 1048576.0));
         }
     }
 }
 
 template <typename real>
 cudaError_t launch_noise(real *grid, uint64_t seed, const int64_t domain[3], const int64_t owned_lo[3],
-                         const int64_t owned_n[3], const int brick[3], const Geom &g, cudaStream_t s)
+                         const int64_t owned_n[3], const int brick[3], const Geom &g, int rep, cudaStream_t s)
 {
     const int64_t ncells = owned_n[0] * owned_n[1] * owned_n[2];
     int64_t nb = (ncells + 255) / 256;
     if (nb > 16384) nb = 16384;
     noise_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, seed, domain[0], domain[1], owned_lo[0], owned_lo[1],
                                                    owned_lo[2], owned_n[0], owned_n[1], ncells, brick[0], brick[1],
-                                                   brick[2], g);
+                                                   brick[2], g, rep);
     return cudaGetLastError();
 }
 
 template <typename real>
 __global__ void gather_kernel(const real *grid, const uint8_t *flags, const int64_t *xyz, int64_t n, int b0,
-                              int b1, int b2, const Geom g, double *out)
+                              int b1, int b2, const Geom g, double *out, const int rep, const real *corr)
 {
     const int brick[3] = {b0, b1, b2};
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, xyz[3 * c], xyz[3 * c + 1], xyz[3 * c + 2], lp, lx, ly, lz);
         const int64_t ci = cell_index(g, lx, ly, lz);
-        const bool fluid = flags[(int64_t)lp * g.fs + ci] == 0;
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const bool fluid = fp[0] == 0;
         const real *gp = grid + (int64_t)lp * g.ps + ci;
-        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? (double)gp[q * g.qs] : 0.0;
+        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
     }
 }
 
 template <typename real>
 cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t *xyz_local, int64_t n,
-                          const int brick[3], const Geom &g, double *out, cudaStream_t s)
+                          const int brick[3], const Geom &g, double *out, int rep, const real *corr, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     int64_t nb = (n + 127) / 128;
     if (nb > 4096) nb = 4096;
-    gather_kernel<real><<<(unsigned)nb, 128, 0, s>>>(grid, flags, xyz_local, n, brick[0], brick[1], brick[2], g, out);
+    gather_kernel<real><<<(unsigned)nb, 128, 0, s>>>(grid, flags, xyz_local, n, brick[0], brick[1], brick[2], g, out,
+                                                     rep, corr);
     return cudaGetLastError();
 }
 
@@ -462,9 +616,11 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
 // wall-adjacent fluid cell x into its wall neighbours: grid_opp(j)(x + e_j) =
 // grid_j(x) + corr.  Needed once after the state or the flags are set; every
 // later step maintains them inside the sweep.
+// aa = 0: two-grid state (wall slot opp(j) <- S_j(x)); aa = 1: AA swapped
+// state (S_j(x) = A[x][opp(j)], wall slot j, as the LOCAL kernel writes it).
 template <typename real>
 __global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr,
-                               const Geom g)
+                               const Geom g, const int aa)
 {
     const int lp = blockIdx.y;
     real *gp = grid + (int64_t)lp * g.ps;
@@ -476,16 +632,16 @@ __global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *
             const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
             const uint8_t f = fp[e + sh];
             if (f == 0) continue;
-            real v = gp[j * g.qs + e];
+            real v = gp[(aa ? OPP(j) : j) * g.qs + e];
             if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
-            gp[OPP(j) * g.qs + e + sh] = v;
+            gp[(aa ? j : OPP(j)) * g.qs + e + sh] = v;
         }
     }
 }
 
 template <typename real>
 cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
-                           const Geom &g, cudaStream_t s)
+                           const Geom &g, int aa, cudaStream_t s)
 {
     int64_t bx = (g.fs + 255) / 256;
     if (bx > 2048) bx = 2048;
@@ -493,27 +649,29 @@ cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind
         int n = nlocal - off < 65535 ? nlocal - off : 65535;
         dim3 grid_dim((unsigned)bx, (unsigned)n);
         bb_fill_kernel<real><<<grid_dim, 256, 0, s>>>(grid + (int64_t)off * g.ps, flags + (int64_t)off * g.fs,
-                                                      kind + (int64_t)off * g.fs, corr, g);
+                                                      kind + (int64_t)off * g.fs, corr, g, aa);
     }
     return cudaGetLastError();
 }
 
 #define LBM_INSTANTIATE(real)                                                                                   \
-    template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, int, cudaStream_t);                    \
+    template cudaError_t launch_sweep<real>(const SweepArgs<real> &, int64_t, int, cudaStream_t);               \
+    template cudaError_t launch_sweep_aa<real>(const SweepArgs<real> &, int64_t, bool, int, cudaStream_t);      \
     template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
                                                     const real *, real *, const uint8_t *, const Geom &,       \
                                                     cudaStream_t);                                             \
     template cudaError_t launch_bb_fill<real>(real *, const uint8_t *, const uint8_t *, const real *, int,      \
-                                              const Geom &, cudaStream_t);                                     \
+                                              const Geom &, int, cudaStream_t);                                \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
-                                             const int *, const Geom &, real *, cudaStream_t);                 \
+                                             const int *, const Geom &, real *, int, cudaStream_t);            \
     template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \
                                              const int64_t *, const int *, const Geom &, double *, int,        \
-                                             double *, double *, cudaStream_t);                                \
+                                             double *, double *, int, const real *, cudaStream_t);             \
     template cudaError_t launch_noise<real>(real *, uint64_t, const int64_t *, const int64_t *, const int64_t *, \
-                                            const int *, const Geom &, cudaStream_t);                          \
+                                            const int *, const Geom &, int, cudaStream_t);                     \
     template cudaError_t launch_gather<real>(const real *, const uint8_t *, const int64_t *, int64_t,            \
-                                             const int *, const Geom &, double *, cudaStream_t);
+                                             const int *, const Geom &, double *, int, const real *,           \
+                                             cudaStream_t);
 
 LBM_INSTANTIATE(float)
 LBM_INSTANTIATE(double)

@@ -51,10 +51,15 @@ cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elem
                                  real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
                                  const Geom &g, cudaStream_t s);
 
-// Store-side bounce-back values of the current state (after set_pdfs / set_flags).
+// Store-side bounce-back values of the current state (after set_pdfs / set_flags);
+// aa = 1: AA swapped representation.
 template <typename real>
 cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
-                           const Geom &g, cudaStream_t s);
+                           const Geom &g, int aa, cudaStream_t s);
+
+// AA-pattern in-place sweeps (kernels.cu): pull = true -> PULL kernel, else LOCAL.
+template <typename real>
+cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s);
 
 // Build per-patch flags (incl. ghosts, periodic wrap) from the global flag
 // array (device copy, (nz+2)(ny+2)(nx+2)), then the per-cell kind.
@@ -63,21 +68,23 @@ cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], c
                                uint8_t *flags, uint8_t *kind, cudaStream_t s);
 
 // Import / export between the canonical double [z][y][x][19] layout of a
-// range of owned z-planes and the patch grids.
+// range of owned z-planes and the patch grids.  rep: 0 two-grid, 1 AA
+// swapped, 2 AA streamed (export / gather only).
 template <typename real>
 cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, const int64_t owned_lo[3],
-                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid,
+                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid, int rep,
                           cudaStream_t s);
 template <typename real>
 cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, int64_t nz_chunk,
                           const int64_t owned_lo[3], const int64_t owned_n[3], const int brick[3],
                           const Geom &g, double *canon, int mode /*0 pdfs, 1 macroscopic*/, double *rho,
-                          double *u, cudaStream_t s);
+                          double *u, int rep, const real *corr, cudaStream_t s);
 template <typename real>
 cudaError_t launch_noise(real *grid, uint64_t seed, const int64_t domain[3], const int64_t owned_lo[3],
-                         const int64_t owned_n[3], const int brick[3], const Geom &g, cudaStream_t s);
+                         const int64_t owned_n[3], const int brick[3], const Geom &g, int rep, cudaStream_t s);
 template <typename real>
 cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t *xyz_local /*3 per cell*/,
-                          int64_t n, const int brick[3], const Geom &g, double *out, cudaStream_t s);
+                          int64_t n, const int brick[3], const Geom &g, double *out, int rep, const real *corr,
+                          cudaStream_t s);
 
 }  // namespace lbm

@@ -70,6 +70,10 @@ struct Box {
 struct CopySeg {
     int64_t src_base, dst_base;
     int64_t dst_flag_base;          // flag offset of the destination patch (grid destinations)
+    int32_t mask;                   // 0: write grid destinations only into fluid cells;
+                                    // 2: AA half-exchange 2 -- additionally the writer cell
+                                    //    y - e_q must be fluid and inside the sender (see plan.cpp)
+    int32_t d[3];                   // direction from the receiving patch to the sending patch
     int32_t src_is_buf, dst_is_buf;
     int32_t src_lo[3], dst_lo[3], size[3];
     int32_t nq;
@@ -121,7 +125,17 @@ struct SegLists {
     std::vector<Seg> send;    // grouped by peer (ascending), canonical order inside
     std::vector<Seg> recv;
 };
-void build_segments(const Decomp &dec, SegLists &out);
+// Exchange kinds (d = direction from the receiving patch to the sending patch):
+//   EX_AB : two-grid pull.  sender boundary layer -> receiver ghost layer,
+//           slots q with e_q[a] = -d[a] (the PDFs the receiver's cells pull).
+//   EX_AA1: AA half-exchange 1 (after the local step).  Same regions, slots
+//           e_q[a] = +d[a] (swapped post-collision values the receiver's next
+//           pull step gathers from its ghost layer).
+//   EX_AA2: AA half-exchange 2 (after the pull step).  sender GHOST layer ->
+//           receiver BOUNDARY layer, slots e_q[a] = -d[a] (what the sender's
+//           cells scattered into their ghost layer belongs to the receiver).
+enum ExKind { EX_AB = 0, EX_AA1 = 1, EX_AA2 = 2 };
+void build_segments(const Decomp &dec, SegLists &out, int kind = EX_AB);
 extern const Dir3 kDirs[NDIR];
 
 }  // namespace lbm

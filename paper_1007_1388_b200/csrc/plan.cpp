@@ -81,6 +81,7 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
     if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks) return "need 0 <= rank < nranks";
     if (cfg.exchange_mode != LBM_EXCHANGE_AUTO && cfg.exchange_mode != LBM_EXCHANGE_FORCE_BUFFERS)
         return "unknown exchange_mode";
+    if (cfg.layout != LBM_LAYOUT_AB && cfg.layout != LBM_LAYOUT_AA) return "unknown layout";
     int pg[3] = {cfg.proc_grid[0], cfg.proc_grid[1], cfg.proc_grid[2]};
     if (pg[0] == 0 && pg[1] == 0 && pg[2] == 0) {
         // Default: split z first, then y, then x.
@@ -137,7 +138,7 @@ static int neighbour(const Decomp &dec, int g, const int d[3])
 // direction index k, the PDFs its boundary cells pull from neighbour `send`.
 // The pulled directions i satisfy e_i[a] = -d[a] on every axis with d[a] != 0
 // (a cell x pulls f_i from x - e_i): 5 for a face, 1 for an edge.
-static Seg make_seg(const Decomp &dec, int recv, int send, int k)
+static Seg make_seg(const Decomp &dec, int recv, int send, int k, int kind)
 {
     Seg s;
     std::memset(&s, 0, sizeof s);
@@ -149,12 +150,13 @@ static Seg make_seg(const Decomp &dec, int recv, int send, int k)
     for (int a = 0; a < 3; ++a) {
         int n = dec.patch[a];
         if (s.d[a] == 1) {
-            s.recv_lo[a] = n;
-            s.send_lo[a] = 0;
+            // receiver ghost at n <- sender boundary at 0 (AA2: receiver boundary n-1 <- sender ghost -1)
+            s.recv_lo[a] = kind == EX_AA2 ? n - 1 : n;
+            s.send_lo[a] = kind == EX_AA2 ? -1 : 0;
             s.size[a] = 1;
         } else if (s.d[a] == -1) {
-            s.recv_lo[a] = -1;
-            s.send_lo[a] = n - 1;
+            s.recv_lo[a] = kind == EX_AA2 ? 0 : -1;
+            s.send_lo[a] = kind == EX_AA2 ? n : n - 1;
             s.size[a] = 1;
         } else {
             s.recv_lo[a] = 0;
@@ -164,17 +166,18 @@ static Seg make_seg(const Decomp &dec, int recv, int send, int k)
         s.cells *= s.size[a];
     }
     s.nq = 0;
+    const int sign = kind == EX_AA1 ? 1 : -1;
     for (int i = 0; i < Q; ++i) {
         const int e[3] = {EX(i), EY(i), EZ(i)};
         bool ok = true;
         for (int a = 0; a < 3; ++a)
-            if (s.d[a] != 0 && e[a] != -s.d[a]) ok = false;
+            if (s.d[a] != 0 && e[a] != sign * s.d[a]) ok = false;
         if (ok && i != 0 && s.nq < 5) s.q[s.nq++] = i;
     }
     return s;
 }
 
-void build_segments(const Decomp &dec, SegLists &out)
+void build_segments(const Decomp &dec, SegLists &out, int kind)
 {
     out.local.clear();
     out.send.clear();
@@ -185,7 +188,7 @@ void build_segments(const Decomp &dec, SegLists &out)
         for (int k = 0; k < NDIR; ++k) {
             int nb = neighbour(dec, g, kDirs[k].d);
             if (nb < 0) continue;
-            Seg s = make_seg(dec, g, nb, k);
+            Seg s = make_seg(dec, g, nb, k, kind);
             int own = dec.owner(nb);
             s.peer = own;
             if (own == dec.rank && !dec.force_buffers)
@@ -207,7 +210,7 @@ void build_segments(const Decomp &dec, SegLists &out)
             int kr = -1;
             for (int j = 0; j < NDIR; ++j)
                 if (kDirs[j].d[0] == minus[0] && kDirs[j].d[1] == minus[1] && kDirs[j].d[2] == minus[2]) kr = j;
-            Seg s = make_seg(dec, p, g, kr);
+            Seg s = make_seg(dec, p, g, kr, kind);
             s.peer = own;
             out.send.push_back(s);
         }

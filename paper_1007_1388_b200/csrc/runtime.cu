@@ -54,6 +54,18 @@ struct Peer {
     int64_t send_off, send_n, recv_off, recv_n;
 };
 
+// One exchange kind (EX_AB, EX_AA1, EX_AA2): segment lists, device copy
+// descriptors and the per-peer message layout.
+struct ExSet {
+    SegLists segs;
+    DevSegs pack_all;   // pack + local copies (non-overlapped step / ghost refresh)
+    DevSegs pack_remote, local_copy, unpack;
+    std::vector<Peer> peers;
+    int64_t send_elems = 0, recv_elems = 0;
+    bool has_remote = false;   // anything goes through buffers
+    bool has_nccl = false;     // a peer other than this rank
+};
+
 struct TimingSlot {
     cudaEvent_t ev[kEvPerSlot];
     bool used = false;
@@ -73,6 +85,7 @@ struct lbm_ctx {
     // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
     // fp32 4 blocks/SM plain stores, fp64 3 blocks/SM evict-first stores; env LBM_SWEEP_VARIANT.
     int sweep_variant[2] = {6, 5};
+    int aa_variant[2] = {6, 2};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
     bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
     int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
     int num_sms = 148;
@@ -87,12 +100,10 @@ struct lbm_ctx {
     uint8_t *flags = nullptr, *kind = nullptr;
     void *corr = nullptr;
     int *d_origin = nullptr;
-    SegLists segs;
-    DevSegs pack_all;   // pack + local copies (non-overlapped step / ghost refresh)
-    DevSegs pack_remote, local_copy, unpack;
+    ExSet ex[3];               // indexed by ExKind
+    int layout = LBM_LAYOUT_AB;
+    int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
     void *sendbuf = nullptr, *recvbuf = nullptr;
-    int64_t send_elems = 0, recv_elems = 0;
-    std::vector<Peer> peers;
     bool has_remote = false;   // anything goes through buffers
     bool has_nccl = false;     // a peer other than this rank
     ncclComm_t nccl = nullptr;
@@ -211,7 +222,9 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
     std::vector<int64_t> prefix(boxes.size() + 1, 0);
     for (size_t i = 0; i < boxes.size(); ++i) {
         const Box &b = boxes[i];
-        const int zc = ctx->use_tma ? 1 : sweep_cells_z(ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]);
+        const int zc = (ctx->use_tma || ctx->layout == LBM_LAYOUT_AA)
+                           ? 1
+                           : sweep_cells_z(ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]);
         int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0)
                         ? (int64_t)b.tiles_x * b.tiles_y * ((b.n[2] + zc - 1) / zc)
                         : 0;
@@ -296,11 +309,11 @@ CopySeg buffer_to_grid(const lbm_ctx *ctx, const Seg &s, int64_t buf_base)
     return c;
 }
 
-// Build exchange plan, buffers and sweep boxes.
-lbm_status setup_exchange(lbm_ctx *ctx)
+// Exchange plan of one kind: peers, message offsets, device copy descriptors.
+lbm_status setup_exset(lbm_ctx *ctx, int kind, bool upload)
 {
-    build_segments(ctx->dec, ctx->segs);
-    // peers
+    ExSet &X = ctx->ex[kind];
+    build_segments(ctx->dec, X.segs, kind);
     std::vector<Peer> peers;
     auto peer_of = [&](int r) -> Peer & {
         for (Peer &p : peers)
@@ -308,8 +321,8 @@ lbm_status setup_exchange(lbm_ctx *ctx)
         peers.push_back(Peer{r, 0, 0, 0, 0});
         return peers.back();
     };
-    for (const Seg &s : ctx->segs.send) peer_of(s.peer).send_n += (int64_t)s.nq * s.cells;
-    for (const Seg &s : ctx->segs.recv) peer_of(s.peer).recv_n += (int64_t)s.nq * s.cells;
+    for (const Seg &s : X.segs.send) peer_of(s.peer).send_n += (int64_t)s.nq * s.cells;
+    for (const Seg &s : X.segs.recv) peer_of(s.peer).recv_n += (int64_t)s.nq * s.cells;
     std::sort(peers.begin(), peers.end(), [](const Peer &a, const Peer &b) { return a.rank < b.rank; });
     int64_t so = 0, ro = 0;
     for (Peer &p : peers) {
@@ -318,17 +331,14 @@ lbm_status setup_exchange(lbm_ctx *ctx)
         so += p.send_n;
         ro += p.recv_n;
     }
-    ctx->peers = peers;
-    ctx->send_elems = so;
-    ctx->recv_elems = ro;
-    ctx->has_remote = so > 0 || ro > 0;
-    ctx->has_nccl = false;
+    X.peers = peers;
+    X.send_elems = so;
+    X.recv_elems = ro;
+    X.has_remote = so > 0 || ro > 0;
+    X.has_nccl = false;
     for (const Peer &p : peers)
-        if (p.rank != ctx->dec.rank) ctx->has_nccl = true;
-    lbm_status st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize);
-    if (st) return st;
-    st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize);
-    if (st) return st;
+        if (p.rank != ctx->dec.rank) X.has_nccl = true;
+    if (!upload) return LBM_OK;
 
     auto peer_send_off = [&](int r) {
         for (const Peer &p : peers)
@@ -340,22 +350,48 @@ lbm_status setup_exchange(lbm_ctx *ctx)
             if (p.rank == r) return p.recv_off;
         return (int64_t)0;
     };
+    auto tag = [&](CopySeg c, const Seg &s) {
+        c.mask = kind == EX_AA2 ? 2 : 0;
+        for (int a = 0; a < 3; ++a) c.d[a] = s.d[a];
+        return c;
+    };
     std::vector<CopySeg> pack_all, pack_remote, local, unpack;
-    for (const Seg &s : ctx->segs.send) {
-        CopySeg c = grid_to_x(ctx, s, true, peer_send_off(s.peer));
+    for (const Seg &s : X.segs.send) {
+        CopySeg c = tag(grid_to_x(ctx, s, true, peer_send_off(s.peer)), s);
         pack_all.push_back(c);
         pack_remote.push_back(c);
     }
-    for (const Seg &s : ctx->segs.local) {
-        CopySeg c = grid_to_x(ctx, s, false, 0);
+    for (const Seg &s : X.segs.local) {
+        CopySeg c = tag(grid_to_x(ctx, s, false, 0), s);
         pack_all.push_back(c);
         local.push_back(c);
     }
-    for (const Seg &s : ctx->segs.recv) unpack.push_back(buffer_to_grid(ctx, s, peer_recv_off(s.peer)));
-    if ((st = upload_segs(ctx, pack_all, ctx->pack_all))) return st;
-    if ((st = upload_segs(ctx, pack_remote, ctx->pack_remote))) return st;
-    if ((st = upload_segs(ctx, local, ctx->local_copy))) return st;
-    if ((st = upload_segs(ctx, unpack, ctx->unpack))) return st;
+    for (const Seg &s : X.segs.recv) unpack.push_back(tag(buffer_to_grid(ctx, s, peer_recv_off(s.peer)), s));
+    lbm_status st;
+    if ((st = upload_segs(ctx, pack_all, X.pack_all))) return st;
+    if ((st = upload_segs(ctx, pack_remote, X.pack_remote))) return st;
+    if ((st = upload_segs(ctx, local, X.local_copy))) return st;
+    if ((st = upload_segs(ctx, unpack, X.unpack))) return st;
+    return LBM_OK;
+}
+
+// Build the exchange plans, message buffers and sweep boxes.
+lbm_status setup_exchange(lbm_ctx *ctx)
+{
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    lbm_status st;
+    if ((st = setup_exset(ctx, EX_AB, !aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA1, aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA2, aa))) return st;
+    int64_t so = 0, ro = 0;
+    for (int k = 0; k < 3; ++k) {
+        so = std::max(so, ctx->ex[k].send_elems);
+        ro = std::max(ro, ctx->ex[k].recv_elems);
+    }
+    ctx->has_remote = ctx->ex[EX_AB].has_remote;
+    ctx->has_nccl = ctx->ex[EX_AB].has_nccl;
+    if ((st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize))) return st;
+    if ((st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize))) return st;
 
     // Sweep boxes.  all: one box per local patch.  Overlap: for patches with
     // remote segments, a shell on every side a remote segment touches (1 cell
@@ -365,7 +401,7 @@ lbm_status setup_exchange(lbm_ctx *ctx)
     const int *n = ctx->g.n;
     const int zero[3] = {0, 0, 0};
     std::vector<int> side(6 * ctx->dec.nlocal, 0);
-    for (const Seg &s : ctx->segs.send) {
+    for (const Seg &s : ctx->ex[EX_AB].segs.send) {
         const int l = ctx->dec.global_to_local(s.send_patch);
         // s.d is the direction from the receiver to this (sending) patch; the
         // sender's boundary layer is on side -s.d.
@@ -426,8 +462,13 @@ template <typename real>
 SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
 {
     SweepArgs<real> a;
-    a.src = (const real *)ctx->grid[ctx->cur];
-    a.dst = (real *)ctx->grid[1 - ctx->cur];
+    if (ctx->layout == LBM_LAYOUT_AA) {  // in place
+        a.src = (const real *)ctx->grid[0];
+        a.dst = (real *)ctx->grid[0];
+    } else {
+        a.src = (const real *)ctx->grid[ctx->cur];
+        a.dst = (real *)ctx->grid[1 - ctx->cur];
+    }
     a.flags = ctx->flags;
     a.kind = ctx->kind;
     a.corr = (const real *)ctx->corr;
@@ -443,7 +484,13 @@ lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
 {
     if (b.tiles == 0) return LBM_OK;
     cudaError_t e;
-    if (ctx->use_tma) {
+    if (ctx->layout == LBM_LAYOUT_AA) {
+        const bool pull = ctx->aa_phase == 0;
+        if (ctx->esize == 8)
+            e = launch_sweep_aa<double>(sweep_args<double>(ctx, b), b.tiles, pull, ctx->aa_variant[1], s);
+        else
+            e = launch_sweep_aa<float>(sweep_args<float>(ctx, b), b.tiles, pull, ctx->aa_variant[0], s);
+    } else if (ctx->use_tma) {
         const CUtensorMap &pm = ctx->tm_pdf[ctx->cur];
         if (ctx->esize == 8)
             e = launch_sweep_tma<double>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
@@ -478,17 +525,17 @@ lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *gri
 
 // Transport of the send buffers: grouped NCCL send/recv per peer;
 // a self-peer (exchange_mode FORCE_BUFFERS) is a device copy.
-lbm_status transport(lbm_ctx *ctx, cudaStream_t s)
+lbm_status transport(lbm_ctx *ctx, const ExSet &X, cudaStream_t s)
 {
     const ncclDataType_t dt = ctx->esize == 8 ? ncclFloat64 : ncclFloat32;
     char *sb = (char *)ctx->sendbuf, *rb = (char *)ctx->recvbuf;
-    for (const Peer &p : ctx->peers)
+    for (const Peer &p : X.peers)
         if (p.rank == ctx->dec.rank && p.send_n > 0)
             CK(cudaMemcpyAsync(rb + p.recv_off * ctx->esize, sb + p.send_off * ctx->esize, p.send_n * ctx->esize,
                                cudaMemcpyDeviceToDevice, s));
-    if (!ctx->has_nccl) return LBM_OK;
+    if (!X.has_nccl) return LBM_OK;
     NK(ncclGroupStart());
-    for (const Peer &p : ctx->peers) {
+    for (const Peer &p : X.peers) {
         if (p.rank == ctx->dec.rank) continue;
         if (p.send_n > 0) NK(ncclSend(sb + p.send_off * ctx->esize, (size_t)p.send_n, dt, p.rank, ctx->nccl, s));
         if (p.recv_n > 0) NK(ncclRecv(rb + p.recv_off * ctx->esize, (size_t)p.recv_n, dt, p.rank, ctx->nccl, s));
@@ -498,21 +545,22 @@ lbm_status transport(lbm_ctx *ctx, cudaStream_t s)
 }
 
 // Ghost refresh of grid `gi` (used after set_pdfs / init and inside the step).
-lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts)
+lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, int kind)
 {
     void *grid = ctx->grid[gi];
+    const ExSet &X = ctx->ex[kind];
     lbm_status st;
-    const bool work = ctx->pack_all.n > 0 || ctx->has_remote || ctx->unpack.n > 0;
+    const bool work = X.pack_all.n > 0 || X.has_remote || X.unpack.n > 0;
     if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
     if (ts) ts->exchange = true;
     if (ts) CK(cudaEventRecord(ts->ev[2], s));
-    if ((st = launch_copy(ctx, ctx->pack_all, grid, grid, nullptr, ctx->sendbuf, s))) return st;
+    if ((st = launch_copy(ctx, X.pack_all, grid, grid, nullptr, ctx->sendbuf, s))) return st;
     if (ts) CK(cudaEventRecord(ts->ev[3], s));
-    if (ctx->has_remote) {
-        if ((st = transport(ctx, s))) return st;
+    if (X.has_remote) {
+        if ((st = transport(ctx, X, s))) return st;
     }
     if (ts) CK(cudaEventRecord(ts->ev[4], s));
-    if ((st = launch_copy(ctx, ctx->unpack, nullptr, grid, ctx->recvbuf, nullptr, s))) return st;
+    if ((st = launch_copy(ctx, X.unpack, nullptr, grid, ctx->recvbuf, nullptr, s))) return st;
     if (ts) CK(cudaEventRecord(ts->ev[5], s));
     return LBM_OK;
 }
@@ -521,13 +569,18 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts)
 // grid and park the store-side bounce-back values in the wall cells.
 lbm_status refresh_state(lbm_ctx *ctx)
 {
-    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr);
+    // AB: ghost layers of the current grid.  AA (swapped state): half-exchange 1,
+    // which is what the next PULL step gathers from the ghost layers.
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB);
     if (st) return st;
     cudaError_t e = ctx->esize == 8
                         ? launch_bb_fill<double>((double *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
-                                                 (const double *)ctx->corr, ctx->dec.nlocal, ctx->g, ctx->stream)
+                                                 (const double *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
+                                                 ctx->stream)
                         : launch_bb_fill<float>((float *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
-                                                (const float *)ctx->corr, ctx->dec.nlocal, ctx->g, ctx->stream);
+                                                (const float *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
+                                                ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "bb_fill", __LINE__);
     ctx->launches += (ctx->dec.nlocal + 65534) / 65535;
     CK(cudaStreamSynchronize(ctx->stream));
@@ -593,41 +646,50 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         ts->exchange = false;
         CK(cudaEventRecord(ts->ev[0], s));
     }
-    const int dsti = 1 - ctx->cur;
+    // AB: grid[cur] -> grid[1-cur], exchange of the pulled PDFs.  AA: in place
+    // on grid[0]; a PULL step is followed by half-exchange 2, a LOCAL step by 1.
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    const int dsti = aa ? 0 : 1 - ctx->cur;
+    const int kind = aa ? (ctx->aa_phase == 0 ? EX_AA2 : EX_AA1) : EX_AB;
+    const ExSet &X = ctx->ex[kind];
     void *dst = ctx->grid[dsti];
     if (!ctx->use_overlap) {
         if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
-        if ((st = exchange_seq(ctx, dsti, s, ts))) return st;
+        if ((st = exchange_seq(ctx, dsti, s, ts, kind))) return st;
     } else {
         cudaStream_t c = ctx->comm_stream;
         // S: shells facing remote neighbours, then pack them.
         if ((st = launch_sweep_set(ctx, ctx->box_shell, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[2], s));
-        if ((st = launch_copy(ctx, ctx->pack_remote, dst, dst, nullptr, ctx->sendbuf, s))) return st;
+        if ((st = launch_copy(ctx, X.pack_remote, dst, dst, nullptr, ctx->sendbuf, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[3], s));
         CK(cudaEventRecord(ts ? ts->ev[10] : ctx->slots[0].ev[10], s));
         // C: transport + unpack while S sweeps the interiors.
         CK(cudaStreamWaitEvent(c, ts ? ts->ev[10] : ctx->slots[0].ev[10], 0));
         if (ts) CK(cudaEventRecord(ts->ev[6], c));
-        if ((st = transport(ctx, c))) return st;
+        if ((st = transport(ctx, X, c))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[7], c));
-        if ((st = launch_copy(ctx, ctx->unpack, nullptr, dst, ctx->recvbuf, nullptr, c))) return st;
+        if ((st = launch_copy(ctx, X.unpack, nullptr, dst, ctx->recvbuf, nullptr, c))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[8], c));
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
-        if ((st = launch_copy(ctx, ctx->local_copy, dst, dst, nullptr, nullptr, s))) return st;
+        if ((st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
         CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
     }
     if (ts) CK(cudaEventRecord(ts->ev[kEvPerSlot - 1], s));
-    ctx->cur = dsti;
+    if (aa)
+        ctx->aa_phase ^= 1;
+    else
+        ctx->cur = dsti;
     ctx->steps += 1;
     return LBM_OK;
 }
 
 lbm_status ensure_graph(lbm_ctx *ctx)
 {
-    const int c = ctx->cur;
+    // AB: one graph per starting grid; AA: one graph, starting from the swapped phase.
+    const int c = ctx->layout == LBM_LAYOUT_AA ? 0 : ctx->cur;
     if (ctx->graph[c]) return LBM_OK;
     cudaGraph_t graph = nullptr;
     const int64_t l0 = ctx->launches, s0 = ctx->steps;
@@ -657,11 +719,13 @@ lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n)
 {
     lbm_status st;
     const bool graphs = ctx->cfg.use_graphs && !ctx->timing;
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
     while (n > 0) {
-        if (graphs && n >= 2) {
+        if (graphs && n >= 2 && !(aa && ctx->aa_phase != 0)) {
             if ((st = ensure_graph(ctx))) return st;
-            CK(cudaGraphLaunch(ctx->graph[ctx->cur], ctx->stream));
-            ctx->launches += ctx->graph_launches[ctx->cur];
+            const int gidx = aa ? 0 : ctx->cur;
+            CK(cudaGraphLaunch(ctx->graph[gidx], ctx->stream));
+            ctx->launches += ctx->graph_launches[gidx];
             ctx->steps += 2;
             n -= 2;
         } else {
@@ -762,8 +826,12 @@ void destroy_ctx(lbm_ctx *ctx)
     for (int i = 0; i < 2; ++i)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    for (ExSet &X : ctx->ex)
+        for (void *p : {(void *)X.pack_all.segs, (void *)X.pack_remote.segs, (void *)X.local_copy.segs,
+                        (void *)X.unpack.segs})
+            if (p) cudaFree(p);
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
-                    ctx->recvbuf, ctx->pack_all.segs, ctx->pack_remote.segs, ctx->local_copy.segs, ctx->unpack.segs,
+                    ctx->recvbuf,
                     ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
                     ctx->box_interior.boxes, ctx->box_interior.prefix};
     for (void *p : ptrs)
@@ -803,14 +871,17 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     ctx->cfg = *cfg;
     ctx->dec = dec;
     ctx->esize = cfg->precision;
+    ctx->layout = cfg->layout;
     if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {
         int v = std::atoi(a);
         if (v >= 0 && v < kSweepVariants) ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
+        if (v >= 0 && v < 8) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
     }
     if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
         if (std::string(a) == "simt") ctx->use_tma = false;
         if (std::string(a) == "tma") ctx->use_tma = true;
     }
+    if (ctx->layout == LBM_LAYOUT_AA) ctx->use_tma = false;  // the AA kernels are SIMT
     if (const char *a = std::getenv("LBM_TMA_SHAPE")) {
         int v = std::atoi(a);
         if (v >= 0 && v <= 2) ctx->tma_variant = v;
@@ -889,17 +960,18 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     // Memory budget check (clean OOM before the big allocations).
     const size_t grid_bytes = (size_t)dec.nlocal * ctx->g.ps * ctx->esize;
     const size_t flag_bytes = (size_t)dec.nlocal * ctx->g.fs;
+    const int ngrids = ctx->layout == LBM_LAYOUT_AA ? 1 : 2;
     {
         size_t freeb = 0, totalb = 0;
-        if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess && 2 * grid_bytes + 2 * flag_bytes > freeb) {
+        if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess && ngrids * grid_bytes + 2 * flag_bytes > freeb) {
             char buf[256];
-            std::snprintf(buf, sizeof buf, "need %.2f GB of device memory for the PDF grids and flags, %.2f GB free",
-                          (2.0 * grid_bytes + 2.0 * flag_bytes) / 1e9, freeb / 1e9);
+            std::snprintf(buf, sizeof buf, "need %.2f GB of device memory for the PDF grid(s) and flags, %.2f GB free",
+                          ((double)ngrids * grid_bytes + 2.0 * flag_bytes) / 1e9, freeb / 1e9);
             ctx->err = buf;
             return bail(LBM_ERR_OOM);
         }
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < ngrids; ++i) {
         if ((st = dev_alloc(ctx, &ctx->grid[i], grid_bytes))) return bail(st);
         if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
     }
@@ -981,6 +1053,9 @@ lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode,
     lbm_status st = dev_alloc(ctx, &stage, (size_t)zc * plane_cells * per_cell);
     if (st) return st;
     const void *grid = ctx->grid[ctx->cur];
+    // representation of the state in the grid (kernels.cu rep_slot / read_state)
+    const int rep = ctx->layout == LBM_LAYOUT_AA ? (to_device || ctx->aa_phase == 0 ? 1 : 2) : 0;
+    if (to_device) ctx->aa_phase = 0;
     cudaError_t e = cudaSuccess;
     for (int64_t z0 = 0; z0 < on[2] && e == cudaSuccess; z0 += zc) {
         const int64_t nzc = std::min(zc, on[2] - z0);
@@ -990,17 +1065,19 @@ lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode,
                                 cudaMemcpyHostToDevice, ctx->stream);
             if (e == cudaSuccess)
                 e = ctx->esize == 8 ? launch_import<double>(stage, z0, nzc, ctx->dec.owned_lo, on, ctx->dec.brick,
-                                                            ctx->g, (double *)grid, ctx->stream)
+                                                            ctx->g, (double *)grid, rep, ctx->stream)
                                     : launch_import<float>(stage, z0, nzc, ctx->dec.owned_lo, on, ctx->dec.brick,
-                                                           ctx->g, (float *)grid, ctx->stream);
+                                                           ctx->g, (float *)grid, rep, ctx->stream);
             ctx->launches += 1;
         } else {
             double *srho = stage, *su = stage + cells;
             e = ctx->esize == 8
                     ? launch_export<double>((const double *)grid, ctx->flags, z0, nzc, ctx->dec.owned_lo, on,
-                                            ctx->dec.brick, ctx->g, stage, mode, srho, su, ctx->stream)
+                                            ctx->dec.brick, ctx->g, stage, mode, srho, su, rep,
+                                            (const double *)ctx->corr, ctx->stream)
                     : launch_export<float>((const float *)grid, ctx->flags, z0, nzc, ctx->dec.owned_lo, on,
-                                           ctx->dec.brick, ctx->g, stage, mode, srho, su, ctx->stream);
+                                           ctx->dec.brick, ctx->g, stage, mode, srho, su, rep,
+                                           (const float *)ctx->corr, ctx->stream);
             ctx->launches += 1;
             if (e == cudaSuccess) {
                 if (mode == 0) {
@@ -1043,6 +1120,7 @@ LBM_API void lbm_config_default(lbm_config *cfg)
     cfg->exchange_mode = LBM_EXCHANGE_AUTO;
     cfg->overlap = 1;
     cfg->use_graphs = 1;
+    cfg->layout = LBM_LAYOUT_AB;
 }
 
 LBM_API lbm_status lbm_create(const int64_t domain[3], const int32_t patch[3], double omega, int32_t precision,
@@ -1077,6 +1155,8 @@ LBM_API lbm_status lbm_set_flags(lbm_ctx *ctx, const uint8_t *flags, const doubl
     CHECK_CTX(ctx);
     const char *m = validate_flags(ctx->dec, flags, wall_u, nvel);
     if (m[0]) return ctx->fail(LBM_ERR_ARG, m);
+    if (ctx->layout == LBM_LAYOUT_AA && ctx->aa_phase != 0)
+        return ctx->fail(LBM_ERR_STATE, "AA layout: set_flags is only valid after an even number of steps");
     CK(cudaStreamSynchronize(ctx->stream));
     lbm_status st = apply_flags(ctx, flags, wall_u, nvel);
     if (st) return st;
@@ -1127,9 +1207,10 @@ LBM_API lbm_status lbm_init_noise(lbm_ctx *ctx, uint64_t seed)
     const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
     cudaError_t e = ctx->esize == 8
                         ? launch_noise<double>((double *)ctx->grid[ctx->cur], seed, d.domain, d.owned_lo, on, d.brick,
-                                               ctx->g, ctx->stream)
+                                               ctx->g, ctx->layout == LBM_LAYOUT_AA ? 1 : 0, ctx->stream)
                         : launch_noise<float>((float *)ctx->grid[ctx->cur], seed, d.domain, d.owned_lo, on, d.brick,
-                                              ctx->g, ctx->stream);
+                                              ctx->g, ctx->layout == LBM_LAYOUT_AA ? 1 : 0, ctx->stream);
+    ctx->aa_phase = 0;
     if (e != cudaSuccess) return ctx->cuda_fail(e, "noise_kernel", __LINE__);
     ctx->launches += 1;
     return refresh_state(ctx);
@@ -1190,10 +1271,16 @@ LBM_API lbm_status lbm_get_pdfs_at(lbm_ctx *ctx, const int64_t *xyz, int64_t n, 
     }
     cudaError_t e = cudaMemcpyAsync(dxyz, loc.data(), loc.size() * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess)
-        e = ctx->esize == 8 ? launch_gather<double>((const double *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
-                                                    ctx->dec.brick, ctx->g, dout, ctx->stream)
-                            : launch_gather<float>((const float *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
-                                                   ctx->dec.brick, ctx->g, dout, ctx->stream);
+    {
+        const int rep = ctx->layout == LBM_LAYOUT_AA ? (ctx->aa_phase == 0 ? 1 : 2) : 0;
+        if (e == cudaSuccess)
+            e = ctx->esize == 8 ? launch_gather<double>((const double *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
+                                                        ctx->dec.brick, ctx->g, dout, rep, (const double *)ctx->corr,
+                                                        ctx->stream)
+                                : launch_gather<float>((const float *)ctx->grid[ctx->cur], ctx->flags, dxyz, n,
+                                                       ctx->dec.brick, ctx->g, dout, rep, (const float *)ctx->corr,
+                                                       ctx->stream);
+    }
     ctx->launches += 1;
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(out, dout, (size_t)n * Q * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
@@ -1251,7 +1338,7 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
 {
     if (!ctx || !out) return LBM_ERR_ARG;
     std::memset(out, 0, sizeof *out);
-    fill_info_decomp(ctx->dec, ctx->esize, ctx->segs, out);
+    fill_info_decomp(ctx->dec, ctx->esize, ctx->ex[EX_AB].segs, out);
     out->fluid_cells_local = ctx->fluid_local;
     out->fluid_cells_global = ctx->fluid_global;
     out->steps_done = ctx->steps;
@@ -1265,6 +1352,8 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
     out->row_pitch_elems = ctx->g.px;
     out->align_bytes = ctx->align;
     out->graphs_active = (ctx->graph[0] || ctx->graph[1]) ? 1 : 0;
+    out->layout = ctx->layout;
+    out->aa_phase = ctx->aa_phase;
     return LBM_OK;
 }
 

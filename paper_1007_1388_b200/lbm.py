@@ -16,6 +16,7 @@ Q = 19
 LBM_FP32, LBM_FP64 = 4, 8
 LBM_FLUID, LBM_NOSLIP, LBM_VELOCITY0 = 0, 1, 2
 LBM_EXCHANGE_AUTO, LBM_EXCHANGE_FORCE_BUFFERS = 0, 1
+LBM_LAYOUT_AB, LBM_LAYOUT_AA = 0, 1
 NCCL_ID_BYTES = 128
 NPHASES = 8
 PHASES = ("sweep", "sweep_shell", "sweep_interior", "pack", "nccl", "unpack", "step", "reserved")
@@ -37,7 +38,8 @@ class LbmConfig(ctypes.Structure):
                 ("precision", ctypes.c_int32), ("periodic", ctypes.c_int32 * 3), ("device", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("proc_grid", ctypes.c_int32 * 3),
                 ("nccl_unique_id", ctypes.c_void_p), ("exchange_mode", ctypes.c_int32),
-                ("overlap", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+                ("overlap", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("layout", ctypes.c_int32)]
 
 
 class LbmInfo(ctypes.Structure):
@@ -52,7 +54,8 @@ class LbmInfo(ctypes.Structure):
                 ("halo_bytes_local_per_step", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("phase_ms", ctypes.c_double * NPHASES),
                 ("phase_count", ctypes.c_int64 * NPHASES), ("row_pitch_elems", ctypes.c_int64),
-                ("align_bytes", ctypes.c_int32), ("graphs_active", ctypes.c_int32)]
+                ("align_bytes", ctypes.c_int32), ("graphs_active", ctypes.c_int32), ("layout", ctypes.c_int32),
+                ("aa_phase", ctypes.c_int32)]
 
     def to_dict(self) -> dict:
         out = {}
@@ -122,7 +125,7 @@ def _ptr(a: np.ndarray) -> ctypes.c_void_p:
 
 def default_config(domain, patch=None, omega=1.0 / 0.65, precision=LBM_FP64, periodic=(0, 0, 0), device=-1,
                    rank=0, nranks=1, proc_grid=(0, 0, 0), exchange_mode=LBM_EXCHANGE_AUTO, overlap=1,
-                   use_graphs=1, stream=None) -> LbmConfig:
+                   use_graphs=1, stream=None, layout=LBM_LAYOUT_AB) -> LbmConfig:
     cfg = LbmConfig()
     _lib.lbm_config_default(ctypes.byref(cfg))
     patch = domain if patch is None else patch
@@ -140,6 +143,7 @@ def default_config(domain, patch=None, omega=1.0 / 0.65, precision=LBM_FP64, per
     cfg.overlap = int(overlap)
     cfg.use_graphs = int(use_graphs)
     cfg.stream = stream
+    cfg.layout = int(layout)
     return cfg
 
 

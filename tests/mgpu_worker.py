@@ -29,12 +29,13 @@ def main():
     fl = inputs.add_obstacles(fl, 0.03, seed=13)
     ok = True
     results = {}
-    for prec in (8, 4):
-        for overlap in (1, 0):
+    combos = [(8, 1, 0), (8, 0, 0), (4, 1, 0), (4, 0, 0), (8, 1, 1), (4, 0, 1)]  # (prec, overlap, AA layout)
+    for prec, overlap, layout in combos:
+        if True:
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, rank=rank, nranks=world,
-                            nccl_id=obj[0], periodic=periodic, overlap=overlap)
+                            nccl_id=obj[0], periodic=periodic, overlap=overlap, layout=layout)
             L.set_flags(fl, wu)
             f0 = inputs.noise_pdfs(domain, L.owned_lo, L.owned_hi)
             L.set_pdfs(f0)
@@ -48,8 +49,8 @@ def main():
                 full = np.zeros((domain[2], domain[1], domain[0], 19))
                 for lo, hi, a in parts:
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
-                results[(prec, overlap)] = full
-                print(f"prec={prec} overlap={overlap} peers={info['peers']} "
+                results[(prec, overlap, layout)] = full
+                print(f"prec={prec} overlap={overlap} layout={layout} peers={info['peers']} "
                       f"halo={info['halo_bytes_remote_per_step']}", flush=True)
     if rank == 0:
         import oracle
@@ -62,11 +63,14 @@ def main():
                 L.set_pdfs(inputs.noise_pdfs(domain))
                 L.step(steps)
                 single = L.get_pdfs()
-            for overlap in (1, 0):
-                same = np.array_equal(results[(prec, overlap)], single)
-                err = float(np.abs(results[(prec, overlap)][mask] - ref[mask]).max())
+            for (p2, overlap, layout), res in results.items():
+                if p2 != prec:
+                    continue
+                same = np.array_equal(res, single)
+                err = float(np.abs(res[mask] - ref[mask]).max())
                 tol = 1e-12 if prec == 8 else 1e-5
-                print(f"prec={prec} overlap={overlap} bitwise_vs_1gpu={same} max|oracle diff|={err:.3e}", flush=True)
+                print(f"prec={prec} overlap={overlap} layout={layout} bitwise_vs_1gpu={same} "
+                      f"max|oracle diff|={err:.3e}", flush=True)
                 ok = ok and same and err <= tol
     flag = torch.tensor([1 if ok else 0])
     dist.broadcast(flag, 0)

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--precisions", default="8,4")
     ap.add_argument("--impls", default="tma,simt")
     ap.add_argument("--shapes", default="0-2")
+    ap.add_argument("--layout", type=int, default=0)
     args = ap.parse_args()
     import torch
     from paper_1007_1388_b200 import inputs, lbm
@@ -53,7 +54,7 @@ def main():
                 os.environ["LBM_SWEEP_VARIANT"] = str(v) if impl == "simt" else "7"
                 os.environ["LBM_TMA_SHAPE"] = str(v) if impl == "tma" else "0"
                 os.environ["LBM_ALIGN_BYTES"] = str(align)
-                L = lbm.Lattice(n, patch, inputs.LDC_OMEGA, prec, device=0)
+                L = lbm.Lattice(n, patch, inputs.LDC_OMEGA, prec, device=0, layout=args.layout)
                 L.set_flags(fl, wu)
                 L.init_noise(1388)
                 L.step(10)
@@ -69,7 +70,8 @@ def main():
                 L.close()
                 mfl = fluid / (ms / 1e3) / 1e6
                 gbs = mfl * 1e6 * 2 * 19 * prec / 1e9
-                r = dict(prec=prec, impl=impl, variant=v, align=align, ms=ms, mflups=mfl, alg_gbs=gbs)
+                r = dict(prec=prec, impl=impl, variant=v, align=align, layout=args.layout, ms=ms, mflups=mfl,
+                         alg_gbs=gbs)
                 results.append(r)
                 print(json.dumps(r), flush=True)
     best = {}
