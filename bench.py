@@ -359,6 +359,9 @@ def main():
             cpu = {"value": None, "unit": "MFLUPS", "cores": 0, "kind": "oracle", "sample": f"failed: {exc}"}
 
     clocks = clk.summary()
+    from paper_1007_1388_b200 import model
+    est = model.b200_step_estimate(L.owned_shape, info["proc_coord"], pgrid, esize, peak,
+                                   overlap=bool(args.overlap))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "MFLUPS", "n_gpus": world, "steps": args.steps,
@@ -375,6 +378,8 @@ def main():
                        "row_pitch_elems": info["row_pitch_elems"], "align_bytes": info["align_bytes"]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks,
+            "model": {"source": "paper_1007_1388_b200/model.py (P:577-613 re-parameterised: HBM roofline + "
+                                "NVLink 770 GB/s halo)", **est},
         }
         print(json.dumps(line), flush=True)
     L.close()
