@@ -208,6 +208,9 @@ def main():
     ap.add_argument("--overlap", type=int, default=1)
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--layout", choices=("ab", "aa"), default="ab")
+    ap.add_argument("--exchange", choices=("fused", "nccl"), default="fused",
+                    help="fused: sweep stores into neighbour ghosts (NVLink peer stores across GPUs); "
+                         "nccl: pack -> NCCL send/recv -> unpack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -232,6 +235,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.exchange == "nccl":
+        os.environ["LBM_EXCHANGE"] = "nccl"
     from paper_1007_1388_b200 import inputs, lbm
 
     prec = lbm.LBM_FP64 if args.precision == "fp64" else lbm.LBM_FP32
@@ -373,6 +378,7 @@ def main():
                        "fluid_cells": fluid_global, "mflups_per_gpu": value / world,
                        "omega": inputs.LDC_OMEGA, "lid_u": inputs.LDC_U, "init": "dyadic noise seed 1388",
                        "overlap": bool(args.overlap), "graphs": bool(args.graphs), "layout": args.layout,
+                       "exchange": "fused" if info["exchange_fused"] else "nccl",
                        "l2": f"no flush: PDF state {2 * 19 * esize * fluid_local / 1e9:.2f} GB/GPU >> 126 MB L2",
                        "halo_bytes_remote_per_step": info["halo_bytes_remote_per_step"],
                        "row_pitch_elems": info["row_pitch_elems"], "align_bytes": info["align_bytes"]},

@@ -146,6 +146,11 @@ typedef struct {
     int32_t graphs_active;
     int32_t layout;                        /* LBM_LAYOUT_*                                  */
     int32_t aa_phase;                      /* AA: 0 swapped (even step count), 1 streamed   */
+    int32_t exchange_fused;                /* 1: the sweep stores outgoing PDFs straight into
+                                              neighbour ghost layers (same GPU: plain stores,
+                                              other GPUs: NVLink stores to CUDA-IPC-mapped
+                                              memory, one epoch handshake per step);
+                                              0: pack -> NCCL / copy -> unpack             */
 } lbm_info;
 
 /* One remote message of the static exchange plan (lbm_plan, host-only).      */

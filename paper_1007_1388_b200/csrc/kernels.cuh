@@ -33,6 +33,25 @@ struct SweepArgs {
 // 2 planes), min blocks 2 / 3, stcs 0 / 1.
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s);
+
+// Sweep fused with the ghost exchange (sweep_direct.cu).
+template <typename real>
+struct DirectArgs {
+    real *const *nbr;                        // [nlocal][18][2]: neighbour patch base in grid i, or null
+    const uint32_t *remote_mask;             // [nlocal]: bit kd = neighbour kd lives on another GPU
+    int dsti;                                // destination grid index (0 / 1)
+    unsigned *cta_count;                     // completion counter, reset by the last CTA
+    unsigned long long *epoch;               // steps completed by this rank
+    unsigned long long *const *peer_inbox;   // [npeers]: &inbox_peer[my rank] (peer-mapped)
+    int npeers;
+};
+template <typename real>
+cudaError_t launch_sweep_direct(const SweepArgs<real> &a, const DirectArgs<real> &dx, int64_t total_tiles,
+                                int variant, cudaStream_t s);
+cudaError_t launch_wait_peers(const unsigned long long *inbox, const int *peer_rank, int npeers,
+                              const unsigned long long *epoch, int *error, cudaStream_t s);
+cudaError_t launch_signal_peers(unsigned long long *epoch, unsigned long long *const *peer_inbox, int npeers,
+                                cudaStream_t s);
 constexpr int kSweepVariants = 12;
 __host__ __device__ constexpr int sweep_cells_z(int variant) { return variant >= 8 ? 2 : 1; }
 

@@ -111,6 +111,7 @@ struct Decomp {
     // local patch l <-> global id; local order = brick-local z, y, x
     int local_to_global(int l) const;
     int global_to_local(int g) const;   // -1 if not owned
+    int local_index_on_owner(int g) const;  // storage index of g on its owning rank
     int owner(int g) const;
     void patch_coord(int g, int c[3]) const;
     int patch_id(const int c[3]) const;
@@ -136,6 +137,8 @@ struct SegLists {
 //           cells scattered into their ghost layer belongs to the receiver).
 enum ExKind { EX_AB = 0, EX_AA1 = 1, EX_AA2 = 2 };
 void build_segments(const Decomp &dec, SegLists &out, int kind = EX_AB);
+// Neighbour patch of global patch g in direction d (periodic wrap), or -1.
+int neighbour(const Decomp &dec, int g, const int d[3]);
 extern const Dir3 kDirs[NDIR];
 
 }  // namespace lbm

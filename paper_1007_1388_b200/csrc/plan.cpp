@@ -119,8 +119,17 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
     return "";
 }
 
+int Decomp::local_index_on_owner(int g) const
+{
+    int c[3];
+    patch_coord(g, c);
+    int b[3];
+    for (int a = 0; a < 3; ++a) b[a] = c[a] % brick[a];
+    return (b[2] * brick[1] + b[1]) * brick[0] + b[0];
+}
+
 // Neighbour patch of global patch g in direction d (periodic wrap), or -1.
-static int neighbour(const Decomp &dec, int g, const int d[3])
+int neighbour(const Decomp &dec, int g, const int d[3])
 {
     int c[3];
     dec.patch_coord(g, c);

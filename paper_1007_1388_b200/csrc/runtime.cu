@@ -85,7 +85,8 @@ struct lbm_ctx {
     // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
     // fp32 4 blocks/SM plain stores, fp64 3 blocks/SM evict-first stores; env LBM_SWEEP_VARIANT.
     int sweep_variant[2] = {6, 5};
-    int aa_variant[2] = {6, 2};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
+    int aa_variant[2] = {6, 2};
+    int direct_variant[2] = {6, 5};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
     bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
     int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
     int num_sms = 148;
@@ -101,6 +102,19 @@ struct lbm_ctx {
     void *corr = nullptr;
     int *d_origin = nullptr;
     ExSet ex[3];               // indexed by ExKind
+    // Fused exchange (sweep_direct.cu): the sweep stores outgoing PDFs straight
+    // into neighbour ghost layers (local or CUDA-IPC-mapped peer memory).
+    bool direct = false;
+    void **d_nbr = nullptr;                 // [nlocal][18][2] neighbour patch bases
+    uint32_t *d_remote_mask = nullptr;      // [nlocal]
+    unsigned *d_cta = nullptr;
+    unsigned long long *d_epoch = nullptr;
+    unsigned long long *d_inbox = nullptr;  // [nranks] epochs published by the peers
+    unsigned long long **d_peer_inbox = nullptr;
+    int *d_peer_rank = nullptr;
+    int *d_error = nullptr;
+    int npeers_direct = 0;
+    std::vector<void *> ipc_mapped;         // peer grids / inboxes opened with cudaIpcOpenMemHandle
     int layout = LBM_LAYOUT_AB;
     int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
     void *sendbuf = nullptr, *recvbuf = nullptr;
@@ -108,6 +122,7 @@ struct lbm_ctx {
     bool has_nccl = false;     // a peer other than this rank
     ncclComm_t nccl = nullptr;
     DevBoxes box_all, box_shell, box_interior;
+    DevBoxes box_direct;   // fused exchange: remote-face shells first, then the rest
     bool use_overlap = false;
     int64_t fluid_local = 0, fluid_global = 0;
     bool flags_set = false;
@@ -454,6 +469,11 @@ lbm_status setup_exchange(lbm_ctx *ctx)
     if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
     if ((st = upload_boxes(ctx, shell, ctx->box_shell))) return st;
     if ((st = upload_boxes(ctx, interior, ctx->box_interior))) return st;
+    {
+        std::vector<Box> direct(shell);
+        direct.insert(direct.end(), interior.begin(), interior.end());
+        if ((st = upload_boxes(ctx, direct, ctx->box_direct))) return st;
+    }
     ctx->use_overlap = ctx->cfg.overlap && ctx->has_nccl;
     return LBM_OK;
 }
@@ -642,7 +662,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         ctx->slot_next = (ctx->slot_next + 1) % kTimingSlots;
         if ((st = accumulate_slot(ctx, *ts))) return st;
         ts->used = true;
-        ts->overlap = ctx->use_overlap;
+        ts->overlap = ctx->use_overlap && !ctx->direct;
         ts->exchange = false;
         CK(cudaEventRecord(ts->ev[0], s));
     }
@@ -653,7 +673,43 @@ lbm_status enqueue_step(lbm_ctx *ctx)
     const int kind = aa ? (ctx->aa_phase == 0 ? EX_AA2 : EX_AA1) : EX_AB;
     const ExSet &X = ctx->ex[kind];
     void *dst = ctx->grid[dsti];
-    if (!ctx->use_overlap) {
+    if (ctx->direct) {
+        // Fused exchange across GPUs.  C (high priority): wait for the peers' epoch,
+        // sweep the shells facing remote neighbours with the fused kernel (NVLink
+        // stores of the outgoing PDFs into the peers' ghost layers), publish the
+        // epoch.  S, concurrently: the plain sweep of everything else.  Then S joins
+        // C and copies the ghosts between same-GPU patches.
+        cudaStream_t c = ctx->comm_stream;
+        cudaEvent_t ev_start = ts ? ts->ev[10] : ctx->slots[0].ev[10];
+        cudaEvent_t ev_shell = ts ? ts->ev[11] : ctx->slots[0].ev[11];
+        CK(cudaEventRecord(ev_start, s));
+        CK(cudaStreamWaitEvent(c, ev_start, 0));
+        cudaError_t e = launch_wait_peers(ctx->d_inbox, ctx->d_peer_rank, ctx->npeers_direct, ctx->d_epoch,
+                                          ctx->d_error, c);
+        if (e != cudaSuccess) return ctx->cuda_fail(e, "wait_peers launch", __LINE__);
+        ctx->launches += 1;
+        const DevBoxes &bs = ctx->box_shell;
+        if (bs.tiles > 0) {
+            if (ctx->esize == 8) {
+                DirectArgs<double> dx{(double *const *)ctx->d_nbr, ctx->d_remote_mask, dsti, ctx->d_cta,
+                                      ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct};
+                e = launch_sweep_direct<double>(sweep_args<double>(ctx, bs), dx, bs.tiles, ctx->direct_variant[1], c);
+            } else {
+                DirectArgs<float> dx{(float *const *)ctx->d_nbr, ctx->d_remote_mask, dsti, ctx->d_cta,
+                                     ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct};
+                e = launch_sweep_direct<float>(sweep_args<float>(ctx, bs), dx, bs.tiles, ctx->direct_variant[0], c);
+            }
+            if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_direct launch", __LINE__);
+            ctx->launches += 1;
+        }
+        e = launch_signal_peers(ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct, c);
+        if (e != cudaSuccess) return ctx->cuda_fail(e, "signal_peers launch", __LINE__);
+        ctx->launches += 1;
+        CK(cudaEventRecord(ev_shell, c));
+        if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
+        CK(cudaStreamWaitEvent(s, ev_shell, 0));
+        if ((st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
+    } else if (!ctx->use_overlap) {
         if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
         if ((st = exchange_seq(ctx, dsti, s, ts, kind))) return st;
     } else {
@@ -826,6 +882,10 @@ void destroy_ctx(lbm_ctx *ctx)
     for (int i = 0; i < 2; ++i)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
+    for (void *p : {(void *)ctx->d_nbr, (void *)ctx->d_remote_mask, (void *)ctx->d_cta, (void *)ctx->d_epoch,
+                    (void *)ctx->d_inbox, (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
+        if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)
         for (void *p : {(void *)X.pack_all.segs, (void *)X.pack_remote.segs, (void *)X.local_copy.segs,
                         (void *)X.unpack.segs})
@@ -833,7 +893,8 @@ void destroy_ctx(lbm_ctx *ctx)
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
                     ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
-                    ctx->box_interior.boxes, ctx->box_interior.prefix};
+                    ctx->box_interior.boxes, ctx->box_interior.prefix, ctx->box_direct.boxes,
+                    ctx->box_direct.prefix};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->events_created)
@@ -843,6 +904,111 @@ void destroy_ctx(lbm_ctx *ctx)
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     cudaGetLastError();
     delete ctx;
+}
+
+// Fused-exchange setup: neighbour pointer table, epoch / inbox buffers and,
+// across GPUs, the CUDA IPC mapping of the peers' grids and inboxes (handles
+// all-gathered over the NCCL communicator).  All ranks agree on the outcome.
+lbm_status setup_direct(lbm_ctx *ctx)
+{
+    const Decomp &dec = ctx->dec;
+    const int R = dec.nranks, me = dec.rank;
+    lbm_status st;
+    if ((st = dev_alloc(ctx, &ctx->d_cta, sizeof(unsigned)))) return st;
+    if ((st = dev_alloc(ctx, &ctx->d_epoch, sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &ctx->d_inbox, (size_t)R * sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &ctx->d_error, sizeof(int)))) return st;
+    CK(cudaMemset(ctx->d_cta, 0, sizeof(unsigned)));
+    CK(cudaMemset(ctx->d_epoch, 0, sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->d_error, 0, sizeof(int)));
+    // Remote peers of the exchange plan.
+    std::vector<int> peers;
+    for (const Peer &p : ctx->ex[EX_AB].peers)
+        if (p.rank != me) peers.push_back(p.rank);
+    if (peers.empty()) return LBM_OK;  // nothing crosses a GPU boundary: copy path
+    std::vector<void *> peer_grid((size_t)R * 2, nullptr), peer_inbox((size_t)R, nullptr);
+    {
+        // all-gather {grid0, grid1, inbox} IPC handles
+        const size_t hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> mine(3);
+        CK(cudaIpcGetMemHandle(&mine[0], ctx->grid[0]));
+        CK(cudaIpcGetMemHandle(&mine[1], ctx->grid[1]));
+        CK(cudaIpcGetMemHandle(&mine[2], ctx->d_inbox));
+        char *dbuf = nullptr;
+        if ((st = dev_alloc(ctx, &dbuf, 3 * hb * (size_t)(R + 1)))) return st;
+        CK(cudaMemcpy(dbuf, mine.data(), 3 * hb, cudaMemcpyHostToDevice));
+        NK(ncclAllGather(dbuf, dbuf + 3 * hb, 3 * hb, ncclUint8, ctx->nccl, ctx->stream));
+        std::vector<cudaIpcMemHandle_t> all((size_t)3 * R);
+        CK(cudaMemcpyAsync(all.data(), dbuf + 3 * hb, 3 * hb * R, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dbuf);
+        ctx->device_bytes -= (int64_t)(3 * hb * (size_t)(R + 1));
+        int ok = 1;
+        for (int r : peers) {
+            for (int i = 0; i < 3 && ok; ++i) {
+                void *ptr = nullptr;
+                if (cudaIpcOpenMemHandle(&ptr, all[(size_t)3 * r + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = 0;
+                    break;
+                }
+                ctx->ipc_mapped.push_back(ptr);
+                if (i < 2)
+                    peer_grid[(size_t)2 * r + i] = ptr;
+                else
+                    peer_inbox[r] = ptr;
+            }
+        }
+        // every rank must take the same path
+        int *dok = nullptr;
+        if ((st = dev_alloc(ctx, &dok, sizeof(int)))) return st;
+        CK(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+        NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->nccl, ctx->stream));
+        CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dok);
+        ctx->device_bytes -= (int64_t)sizeof(int);
+        if (!ok) return LBM_OK;  // stay on the NCCL exchange
+    }
+    // neighbour table
+    const int nl = dec.nlocal;
+    std::vector<void *> nbr((size_t)nl * NDIR * 2, nullptr);
+    std::vector<uint32_t> rmask(nl, 0);
+    for (int l = 0; l < nl; ++l) {
+        const int gpatch = dec.local_to_global(l);
+        for (int k = 0; k < NDIR; ++k) {
+            const int nbp = neighbour(dec, gpatch, kDirs[k].d);
+            if (nbp < 0) continue;
+            const int r = dec.owner(nbp);
+            if (r == me) continue;  // same-GPU neighbours: ghost copy after the sweep
+            const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+            for (int i = 0; i < 2; ++i) {
+                char *base = (char *)peer_grid[(size_t)2 * r + i];
+                nbr[((size_t)l * NDIR + k) * 2 + i] = base + off;
+            }
+            rmask[l] |= 1u << k;
+        }
+    }
+    if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
+    CK(cudaMemcpy(ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    if ((st = dev_alloc(ctx, &ctx->d_remote_mask, rmask.size() * sizeof(uint32_t)))) return st;
+    CK(cudaMemcpy(ctx->d_remote_mask, rmask.data(), rmask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    std::vector<unsigned long long *> pin;
+    std::vector<int> prank;
+    for (int r : peers) {
+        pin.push_back((unsigned long long *)peer_inbox[r] + me);
+        prank.push_back(r);
+    }
+    ctx->npeers_direct = (int)peers.size();
+    if (!peers.empty()) {
+        if ((st = dev_alloc(ctx, &ctx->d_peer_inbox, pin.size() * sizeof(void *)))) return st;
+        CK(cudaMemcpy(ctx->d_peer_inbox, pin.data(), pin.size() * sizeof(void *), cudaMemcpyHostToDevice));
+        if ((st = dev_alloc(ctx, &ctx->d_peer_rank, prank.size() * sizeof(int)))) return st;
+        CK(cudaMemcpy(ctx->d_peer_rank, prank.data(), prank.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    ctx->direct = true;
+    return LBM_OK;
 }
 
 lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
@@ -876,6 +1042,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         int v = std::atoi(a);
         if (v >= 0 && v < kSweepVariants) ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
         if (v >= 0 && v < 8) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
+        if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
     }
     if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
         if (std::string(a) == "simt") ctx->use_tma = false;
@@ -1019,6 +1186,14 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             ctx->err = std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r);
             return bail(LBM_ERR_NCCL);
         }
+    }
+    {
+        // Fused exchange for the two-grid layout unless the NCCL path is requested
+        // (exchange_mode FORCE_BUFFERS, or env LBM_EXCHANGE=nccl).
+        const char *ev = std::getenv("LBM_EXCHANGE");
+        const bool want = ctx->layout == LBM_LAYOUT_AB && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
+                          !(ev && std::string(ev) == "nccl");
+        if (want && (st = setup_direct(ctx))) return bail(st);
     }
     // Default geometry: closed no-slip box at rest (f~ = 0).
     {
@@ -1228,6 +1403,11 @@ LBM_API lbm_status lbm_synchronize(lbm_ctx *ctx)
     CHECK_CTX(ctx);
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaStreamSynchronize(ctx->comm_stream));
+    if (ctx->d_error && ctx->npeers_direct > 0) {
+        int err = 0;
+        CK(cudaMemcpy(&err, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
+        if (err) return ctx->fail(LBM_ERR_INTERNAL, "fused exchange: a peer GPU did not reach the step barrier");
+    }
     if (ctx->timing) return flush_timing(ctx);
     return LBM_OK;
 }
@@ -1354,6 +1534,7 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
     out->graphs_active = (ctx->graph[0] || ctx->graph[1]) ? 1 : 0;
     out->layout = ctx->layout;
     out->aa_phase = ctx->aa_phase;
+    out->exchange_fused = ctx->direct ? 1 : 0;
     return LBM_OK;
 }
 

@@ -29,8 +29,15 @@ def main():
     fl = inputs.add_obstacles(fl, 0.03, seed=13)
     ok = True
     results = {}
-    combos = [(8, 1, 0), (8, 0, 0), (4, 1, 0), (4, 0, 0), (8, 1, 1), (4, 0, 1)]  # (prec, overlap, AA layout)
-    for prec, overlap, layout in combos:
+    # (prec, overlap, layout, exchange): AB uses the fused sweep + NVLink peer stores
+    # by default; "nccl" forces pack -> NCCL -> unpack (LBM_EXCHANGE=nccl)
+    combos = [(8, 1, 0, "fused"), (4, 1, 0, "fused"), (8, 1, 0, "nccl"), (8, 0, 0, "nccl"), (4, 1, 0, "nccl"),
+              (8, 1, 1, "nccl"), (4, 0, 1, "nccl")]
+    for prec, overlap, layout, exch in combos:
+        if exch == "nccl":
+            os.environ["LBM_EXCHANGE"] = "nccl"
+        else:
+            os.environ.pop("LBM_EXCHANGE", None)
         if True:
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -49,8 +56,9 @@ def main():
                 full = np.zeros((domain[2], domain[1], domain[0], 19))
                 for lo, hi, a in parts:
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
-                results[(prec, overlap, layout)] = full
-                print(f"prec={prec} overlap={overlap} layout={layout} peers={info['peers']} "
+                results[(prec, overlap, layout, exch)] = full
+                assert info["exchange_fused"] == (1 if exch == "fused" else 0), info["exchange_fused"]
+                print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} peers={info['peers']} "
                       f"halo={info['halo_bytes_remote_per_step']}", flush=True)
     if rank == 0:
         import oracle
@@ -63,13 +71,13 @@ def main():
                 L.set_pdfs(inputs.noise_pdfs(domain))
                 L.step(steps)
                 single = L.get_pdfs()
-            for (p2, overlap, layout), res in results.items():
+            for (p2, overlap, layout, exch), res in results.items():
                 if p2 != prec:
                     continue
                 same = np.array_equal(res, single)
                 err = float(np.abs(res[mask] - ref[mask]).max())
                 tol = 1e-12 if prec == 8 else 1e-5
-                print(f"prec={prec} overlap={overlap} layout={layout} bitwise_vs_1gpu={same} "
+                print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} bitwise_vs_1gpu={same} "
                       f"max|oracle diff|={err:.3e}", flush=True)
                 ok = ok and same and err <= tol
     flag = torch.tensor([1 if ok else 0])
