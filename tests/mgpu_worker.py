@@ -31,9 +31,14 @@ def main():
     results = {}
     # (prec, overlap, layout, exchange): AB uses the fused sweep + NVLink peer stores
     # by default; "nccl" forces pack -> NCCL -> unpack (LBM_EXCHANGE=nccl)
-    combos = [(8, 1, 0, "fused"), (4, 1, 0, "fused"), (8, 1, 0, "nccl"), (8, 0, 0, "nccl"), (4, 1, 0, "nccl"),
-              (8, 1, 1, "nccl"), (4, 0, 1, "nccl")]
-    for prec, overlap, layout, exch in combos:
+    # plus process grids that split x (the driver's 8-GPU run is 2x2x2)
+    grids = {2: [(0, 0, 0), (2, 1, 1)], 4: [(0, 0, 0), (2, 2, 1), (2, 1, 2)]}.get(world, [(0, 0, 0)])
+    combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "nccl", grids[0]),
+              (8, 0, 0, "nccl", grids[0]), (4, 1, 0, "nccl", grids[0]), (8, 1, 1, "nccl", grids[0]),
+              (4, 0, 1, "nccl", grids[0])]
+    for pg in grids[1:]:
+        combos += [(8, 1, 0, "fused", pg), (8, 1, 0, "nccl", pg), (8, 1, 1, "nccl", pg)]
+    for prec, overlap, layout, exch, pgrid in combos:
         if exch == "nccl":
             os.environ["LBM_EXCHANGE"] = "nccl"
         else:
@@ -42,7 +47,7 @@ def main():
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, rank=rank, nranks=world,
-                            nccl_id=obj[0], periodic=periodic, overlap=overlap, layout=layout)
+                            nccl_id=obj[0], periodic=periodic, overlap=overlap, layout=layout, proc_grid=pgrid)
             L.set_flags(fl, wu)
             f0 = inputs.noise_pdfs(domain, L.owned_lo, L.owned_hi)
             L.set_pdfs(f0)
@@ -56,7 +61,7 @@ def main():
                 full = np.zeros((domain[2], domain[1], domain[0], 19))
                 for lo, hi, a in parts:
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
-                results[(prec, overlap, layout, exch)] = full
+                results[(prec, overlap, layout, exch, tuple(pgrid))] = full
                 assert info["exchange_fused"] == (1 if exch == "fused" else 0), info["exchange_fused"]
                 print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} peers={info['peers']} "
                       f"halo={info['halo_bytes_remote_per_step']}", flush=True)
@@ -71,13 +76,13 @@ def main():
                 L.set_pdfs(inputs.noise_pdfs(domain))
                 L.step(steps)
                 single = L.get_pdfs()
-            for (p2, overlap, layout, exch), res in results.items():
+            for (p2, overlap, layout, exch, pgrid), res in results.items():
                 if p2 != prec:
                     continue
                 same = np.array_equal(res, single)
                 err = float(np.abs(res[mask] - ref[mask]).max())
                 tol = 1e-12 if prec == 8 else 1e-5
-                print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} bitwise_vs_1gpu={same} "
+                print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} grid={pgrid} bitwise_vs_1gpu={same} "
                       f"max|oracle diff|={err:.3e}", flush=True)
                 ok = ok and same and err <= tol
     flag = torch.tensor([1 if ok else 0])
