@@ -151,6 +151,8 @@ typedef struct {
                                               other GPUs: NVLink stores to CUDA-IPC-mapped
                                               memory, one epoch handshake per step);
                                               0: pack -> NCCL / copy -> unpack             */
+    int32_t local_pull;                    /* 1: face cells read same-GPU neighbour patches
+                                              directly (no ghost copies between them)      */
 } lbm_info;
 
 /* One remote message of the static exchange plan (lbm_plan, host-only).      */

@@ -119,6 +119,99 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
     }
 }
 
+// 27 -> 18 neighbour-direction index (plan.cpp kDirs order; -1: centre / corner).
+__constant__ int8_t c_dir27[27] = {-1, 0,  -1, 1,  2,  3,  -1, 4,  -1, 5,  6,  7,  8, -1,
+                                   9,  10, 11, 12, -1, 13, -1, 14, 15, 16, -1, 17, -1};
+
+// Two-grid sweep whose face cells pull across patch boundaries straight from
+// the same-GPU neighbour patch: no ghost copy between
+// local patches.  A source cell x - e_i outside the patch belongs to the
+// neighbour in direction (ox, oy, oz) and sits at (x - e_i) - (ox, oy, oz) * n
+// in its coordinates.  Wall sources keep the store-side bounce-back value of the
+// patch's own ghost layer; remote neighbours keep the exchanged ghosts.
+template <typename real, int MINB, int STCS>
+__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_lp_kernel(const SweepArgs<real> a)
+{
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    // The tile's patch neighbours, indexed by (oz+1)*9 + (oy+1)*3 + (ox+1).
+    __shared__ const real *tab[27];
+    const int tid = threadIdx.y * SWEEP_BX + threadIdx.x;
+    if (tid < 27) {
+        const int kd = c_dir27[tid];
+        tab[tid] = kd < 0 ? nullptr : a.lnbr[((int64_t)bx.patch * NDIR + kd) * 2 + a.srci];
+    }
+    __syncthreads();
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    const int x = bx.lo[0] + tx * SWEEP_BX + (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    if (x >= bx.lo[0] + bx.n[0] || y >= bx.lo[1] + bx.n[1]) return;
+
+    const Geom &g = a.g;
+    const int64_t qs = g.qs;
+    const int64_t cell = cell_index(g, x, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k = a.kind[fbase];
+    const real *s = a.src + pbase;
+    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+    // y / z faces are uniform over a warp (32 consecutive x of one row); an x face
+    // is one lane, whose e_x != 0 directions are redirected by predication.
+    const bool xlo = x == 0, xhi = x == n0 - 1;
+    const int oyl = y == 0 ? -1 : 0, oyh = y == n1 - 1 ? 1 : 0;
+    const int ozl = z == 0 ? -1 : 0, ozh = z == n2 - 1 ? 1 : 0;
+    real p[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+        const real *addr = s + i * qs - sh;
+        const int ox = EX(i) == 1 ? (xlo ? -1 : 0) : (EX(i) == -1 ? (xhi ? 1 : 0) : 0);
+        const int oy = EY(i) == 1 ? oyl : (EY(i) == -1 ? oyh : 0);
+        const int oz = EZ(i) == 1 ? ozl : (EZ(i) == -1 ? ozh : 0);
+        if (ox | oy | oz) {
+            const real *nb = tab[(oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)];
+            if (nb && (k == 0 || a.flags[fbase - sh] == 0))
+                addr = nb + i * qs + cell_index(g, x - EX(i) - ox * n0, y - EY(i) - oy * n1, z - EZ(i) - oz * n2);
+        }
+        p[i] = ld_stream(addr);
+    }
+    if (k == 2) return;
+    uint8_t nbf[Q];
+    if (k == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            nbf[j] = a.flags[fbase + sh];
+        }
+    }
+    collide_bgk<real>(p, a.omega);
+    real *d = a.dst + pbase;
+#pragma unroll
+    for (int i = 0; i < Q; ++i) st_stream<real, STCS>(d + i * qs, p[i]);
+    if (k == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            if (nbf[j] != 0) {
+                const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                real v = p[j];
+                if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
+                d[OPP(j) * qs + sh] = v;
+            }
+        }
+    }
+}
+
 // variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first
 // stores, one cell per thread; 8..11: two cells per thread along z.
 // ------------------------------------------------------------------ AA pattern
@@ -248,6 +341,15 @@ cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int vari
     if (total_tiles <= 0) return cudaSuccess;
     dim3 block(SWEEP_BX, SWEEP_BY, 1);
     const unsigned grid = (unsigned)total_tiles;
+    if (a.lnbr && variant >= 4 && variant < 8) {
+        switch (variant) {
+        case 4: sweep_lp_kernel<real, 3, 0><<<grid, block, 0, s>>>(a); break;
+        case 5: sweep_lp_kernel<real, 3, 1><<<grid, block, 0, s>>>(a); break;
+        case 6: sweep_lp_kernel<real, 4, 0><<<grid, block, 0, s>>>(a); break;
+        default: sweep_lp_kernel<real, 4, 1><<<grid, block, 0, s>>>(a); break;
+        }
+        return cudaGetLastError();
+    }
     switch (variant) {
     case 0: sweep_kernel<real, 1, 0, 1><<<grid, block, 0, s>>>(a); break;
     case 1: sweep_kernel<real, 1, 1, 1><<<grid, block, 0, s>>>(a); break;
@@ -274,16 +376,16 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs,
                                                             real *buf_dst, const uint8_t *flags, const Geom g)
 {
     const CopySeg &sg = segs[blockIdx.y];
-    const int64_t nelem = sg.nelem, cells = sg.cells;
+    // 32-bit element decomposition (a segment has < 2^31 elements).
+    const int nelem = (int)sg.nelem, cells = (int)sg.cells;
     const int s0 = sg.size[0], s1 = sg.size[1];
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nelem;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int qi = (int)(e / cells);
-        const int64_t c = e - (int64_t)qi * cells;
-        const int cx = (int)(c % s0);
-        const int64_t r = c / s0;
-        const int cy = (int)(r % s1);
-        const int cz = (int)(r / s1);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nelem; e += gridDim.x * blockDim.x) {
+        const int qi = e / cells;
+        const int c = e - qi * cells;
+        const int r = c / s0;
+        const int cx = c - r * s0;
+        const int cz = r / s1;
+        const int cy = r - cz * s1;
         const int q = sg.q[qi];
         real v;
         if (sg.src_is_buf)
@@ -296,7 +398,7 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs,
         } else {
             const int y[3] = {sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz};
             const int64_t ci = cell_index(g, y[0], y[1], y[2]);
-            bool ok = flags[sg.dst_flag_base + ci] == 0;
+            bool ok = sg.mask == 1 || flags[sg.dst_flag_base + ci] == 0;  // mask 1: all destinations fluid
             if (sg.mask == 2 && ok) {
                 // AA half-exchange 2: the value was scattered by the sender's cell
                 // w = y - e_q; only entries whose writer is a fluid cell of the

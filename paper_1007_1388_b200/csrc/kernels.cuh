@@ -26,6 +26,11 @@ struct SweepArgs {
     const Box *boxes;       // device
     const int64_t *tile_prefix; // device, nboxes + 1
     int nboxes;
+    // Local pull (NEXT-2): [nlocal][18][2] base of the same-GPU neighbour patch in
+    // grid i (null: no local neighbour); face cells pull from it directly instead
+    // of from a ghost copy.  lnbr == nullptr disables it.
+    const real *const *lnbr = nullptr;
+    int srci = 0;
 };
 
 // variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first stores,

@@ -71,6 +71,7 @@ struct CopySeg {
     int64_t src_base, dst_base;
     int64_t dst_flag_base;          // flag offset of the destination patch (grid destinations)
     int32_t mask;                   // 0: write grid destinations only into fluid cells;
+                                    // 1: every destination cell is fluid (no check);
                                     // 2: AA half-exchange 2 -- additionally the writer cell
                                     //    y - e_q must be fluid and inside the sender (see plan.cpp)
     int32_t d[3];                   // direction from the receiving patch to the sending patch

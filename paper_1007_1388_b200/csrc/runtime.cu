@@ -60,6 +60,7 @@ struct ExSet {
     SegLists segs;
     DevSegs pack_all;   // pack + local copies (non-overlapped step / ghost refresh)
     DevSegs pack_remote, local_copy, unpack;
+    std::vector<CopySeg> h_pack_all, h_local, h_unpack;  // host copies (flag masks are refreshed)
     std::vector<Peer> peers;
     int64_t send_elems = 0, recv_elems = 0;
     bool has_remote = false;   // anything goes through buffers
@@ -115,6 +116,10 @@ struct lbm_ctx {
     int *d_error = nullptr;
     int npeers_direct = 0;
     std::vector<void *> ipc_mapped;         // peer grids / inboxes opened with cudaIpcOpenMemHandle
+    // Local pull (NEXT-2): face cells read same-GPU neighbour patches directly;
+    // no ghost copies between local patches.
+    bool lpull = false;
+    void **d_lnbr = nullptr;                // [nlocal][18][2]
     int layout = LBM_LAYOUT_AB;
     int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
     void *sendbuf = nullptr, *recvbuf = nullptr;
@@ -387,6 +392,49 @@ lbm_status setup_exset(lbm_ctx *ctx, int kind, bool upload)
     if ((st = upload_segs(ctx, pack_remote, X.pack_remote))) return st;
     if ((st = upload_segs(ctx, local, X.local_copy))) return st;
     if ((st = upload_segs(ctx, unpack, X.unpack))) return st;
+    X.h_pack_all = pack_all;
+    X.h_local = local;
+    X.h_unpack = unpack;
+    return LBM_OK;
+}
+
+// After set_flags: a grid-destination segment whose destination cells are all
+// fluid needs no per-element flag check (mask 1).  The checks are half the DRAM
+// reads of the copy kernel on strided x faces (profiles/r01_ncu_copy_*).
+lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
+{
+    const Decomp &d = ctx->dec;
+    const int64_t NX = d.domain[0], NY = d.domain[1], NZ = d.domain[2];
+    auto all_fluid = [&](const CopySeg &c) {
+        const int l = (int)(c.dst_base / ctx->g.ps);
+        int pc[3];
+        d.patch_coord(d.local_to_global(l), pc);
+        for (int z = 0; z < c.size[2]; ++z)
+            for (int y = 0; y < c.size[1]; ++y)
+                for (int x = 0; x < c.size[0]; ++x) {
+                    int64_t gc[3] = {(int64_t)pc[0] * d.patch[0] + c.dst_lo[0] + x,
+                                     (int64_t)pc[1] * d.patch[1] + c.dst_lo[1] + y,
+                                     (int64_t)pc[2] * d.patch[2] + c.dst_lo[2] + z};
+                    const int64_t N[3] = {NX, NY, NZ};
+                    for (int a = 0; a < 3; ++a)
+                        if (d.periodic[a]) gc[a] = (gc[a] % N[a] + N[a]) % N[a];
+                    if (gflags[((gc[2] + 1) * (NY + 2) + (gc[1] + 1)) * (NX + 2) + (gc[0] + 1)] != 0) return false;
+                }
+        return true;
+    };
+    for (int k = 0; k < 3; ++k) {
+        ExSet &X = ctx->ex[k];
+        if (k == EX_AA2) continue;  // its mask also involves the writer cells
+        std::vector<CopySeg> *hv[3] = {&X.h_pack_all, &X.h_local, &X.h_unpack};
+        DevSegs *dv[3] = {&X.pack_all, &X.local_copy, &X.unpack};
+        for (int j = 0; j < 3; ++j) {
+            std::vector<CopySeg> &v = *hv[j];
+            if (v.empty() || !dv[j]->segs) continue;
+            for (CopySeg &c : v)
+                if (!c.dst_is_buf) c.mask = all_fluid(c) ? 1 : 0;
+            CK(cudaMemcpy(dv[j]->segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+        }
+    }
     return LBM_OK;
 }
 
@@ -497,6 +545,8 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.boxes = b.boxes;
     a.tile_prefix = b.prefix;
     a.nboxes = b.n;
+    a.lnbr = ctx->lpull ? (const real *const *)ctx->d_lnbr : nullptr;
+    a.srci = ctx->cur;
     return a;
 }
 
@@ -570,11 +620,13 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, in
     void *grid = ctx->grid[gi];
     const ExSet &X = ctx->ex[kind];
     lbm_status st;
-    const bool work = X.pack_all.n > 0 || X.has_remote || X.unpack.n > 0;
+    const bool work = (ctx->lpull ? X.pack_remote.n : X.pack_all.n) > 0 || X.has_remote || X.unpack.n > 0;
     if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
     if (ts) ts->exchange = true;
     if (ts) CK(cudaEventRecord(ts->ev[2], s));
-    if ((st = launch_copy(ctx, X.pack_all, grid, grid, nullptr, ctx->sendbuf, s))) return st;
+    // local pull: same-GPU neighbours are read in place, only remote segments move
+    if ((st = launch_copy(ctx, ctx->lpull ? X.pack_remote : X.pack_all, grid, grid, nullptr, ctx->sendbuf, s)))
+        return st;
     if (ts) CK(cudaEventRecord(ts->ev[3], s));
     if (X.has_remote) {
         if ((st = transport(ctx, X, s))) return st;
@@ -730,7 +782,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
-        if ((st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
+        if (!ctx->lpull && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
         CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
     }
     if (ts) CK(cudaEventRecord(ts->ev[kEvPerSlot - 1], s));
@@ -822,6 +874,10 @@ lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u,
         std::vector<float> cf(cd.begin(), cd.end());
         CK(cudaMemcpy(ctx->corr, cf.data(), cf.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
+    {
+        lbm_status st2 = update_seg_masks(ctx, flags);
+        if (st2) return st2;
+    }
     // Fluid cell counts (MFLUPS counts fluid cells, R16).
     int64_t gl = 0, lo = 0;
     for (int64_t z = 0; z < nz; ++z)
@@ -883,7 +939,7 @@ void destroy_ctx(lbm_ctx *ctx)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->d_nbr, (void *)ctx->d_remote_mask, (void *)ctx->d_cta, (void *)ctx->d_epoch,
+    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_nbr, (void *)ctx->d_remote_mask, (void *)ctx->d_cta, (void *)ctx->d_epoch,
                     (void *)ctx->d_inbox, (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
         if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)
@@ -1194,6 +1250,32 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         const bool want = ctx->layout == LBM_LAYOUT_AB && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
                           !(ev && std::string(ev) == "nccl");
         if (want && (st = setup_direct(ctx))) return bail(st);
+    }
+    {
+        // Local pull for the SIMT two-grid sweep when same-GPU neighbours exist.
+        // Opt-in: measured slower than the ghost copies on B200.
+        const char *ev = std::getenv("LBM_LOCAL_PULL");
+        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
+        const bool want = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && !ctx->direct &&
+                          cfg->exchange_mode == LBM_EXCHANGE_AUTO && v >= 4 && v < 8 &&
+                          (ev && std::string(ev) == "1") && !ctx->ex[EX_AB].segs.local.empty();
+        if (want) {
+            std::vector<void *> tab((size_t)dec.nlocal * NDIR * 2, nullptr);
+            for (int l = 0; l < dec.nlocal; ++l) {
+                const int gp = dec.local_to_global(l);
+                for (int k = 0; k < NDIR; ++k) {
+                    const int nbp = neighbour(dec, gp, kDirs[k].d);
+                    if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
+                    const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
+                }
+            }
+            if ((st = dev_alloc(ctx, &ctx->d_lnbr, tab.size() * sizeof(void *)))) return bail(st);
+            if (cudaMemcpy(ctx->d_lnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+                return bail(LBM_ERR_CUDA);
+            ctx->lpull = true;
+        }
     }
     // Default geometry: closed no-slip box at rest (f~ = 0).
     {
@@ -1535,6 +1617,8 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
     out->layout = ctx->layout;
     out->aa_phase = ctx->aa_phase;
     out->exchange_fused = ctx->direct ? 1 : 0;
+    out->local_pull = ctx->lpull ? 1 : 0;
+    if (ctx->lpull) out->halo_bytes_local_per_step = 0;
     return LBM_OK;
 }
 

@@ -255,3 +255,28 @@ def test_tma_and_simt_sweeps_bitwise_equal(prec, monkeypatch):
     np.testing.assert_array_equal(out["tma"], out["simt"])
     ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 13, periodic=(0, 1, 0), nthreads=oracle.max_threads())
     assert max_fluid_diff(out["tma"], ref, fl) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_local_pull_equals_ghost_copies(prec, monkeypatch):
+    """Face cells reading same-GPU neighbour patches directly (local pull, NEXT-2)
+    give bitwise the ghost-copy result: 4x3x2 patches, periodic x and z, obstacles
+    on patch boundaries, two moving walls."""
+    n = (64, 30, 24)
+    fl, wu = inputs.ldc_flags(n, periodic=(1, 0, 1))
+    fl = inputs.add_obstacles(fl, 0.06, seed=23, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.0, 0.01, 0.02]]])
+    f0 = inputs.noise_pdfs(n, seed=29)
+    out = {}
+    for lp in ("1", "0"):
+        monkeypatch.setenv("LBM_LOCAL_PULL", lp)
+        L = lbm().Lattice(n, (16, 10, 12), inputs.LDC_OMEGA, prec, periodic=(1, 0, 1))
+        assert L.info()["local_pull"] == int(lp)
+        L.set_flags(fl, wu)
+        L.set_pdfs(f0)
+        L.step(11)
+        out[lp] = L.get_pdfs()
+        L.close()
+    np.testing.assert_array_equal(out["1"], out["0"])
+    one = run_gpu(n, fl, wu, f0, 11, prec, periodic=(1, 0, 1))
+    np.testing.assert_array_equal(out["1"], one)
