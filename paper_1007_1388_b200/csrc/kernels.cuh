@@ -57,8 +57,10 @@ cudaError_t launch_wait_peers(const unsigned long long *inbox, const int *peer_r
                               const unsigned long long *epoch, int *error, cudaStream_t s);
 cudaError_t launch_signal_peers(unsigned long long *epoch, unsigned long long *const *peer_inbox, int npeers,
                                 cudaStream_t s);
-constexpr int kSweepVariants = 12;
-__host__ __device__ constexpr int sweep_cells_z(int variant) { return variant >= 8 ? 2 : 1; }
+// variants 12..15 (fp32 only): two cells per thread along x, float2 accesses,
+// min blocks 4 / 5 of 128 threads, stcs 0 / 1.
+constexpr int kSweepVariants = 16;
+__host__ __device__ constexpr int sweep_cells_z(int variant) { return (variant >= 8 && variant < 12) ? 2 : 1; }
 
 // TMA-staged persistent sweep (sweep_tma.cu); variant selects the tile shape.
 template <typename real>

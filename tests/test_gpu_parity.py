@@ -268,6 +268,7 @@ def test_local_pull_equals_ghost_copies(prec, monkeypatch):
     wu = np.vstack([wu, [[0.0, 0.01, 0.02]]])
     f0 = inputs.noise_pdfs(n, seed=29)
     out = {}
+    monkeypatch.setenv("LBM_SWEEP_VARIANT", "5" if prec == 8 else "6")  # local pull is a 1-cell SIMT variant
     for lp in ("1", "0"):
         monkeypatch.setenv("LBM_LOCAL_PULL", lp)
         L = lbm().Lattice(n, (16, 10, 12), inputs.LDC_OMEGA, prec, periodic=(1, 0, 1))
