@@ -119,16 +119,22 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
     }
 }
 
-// fp32 sweep with two cells per thread along x: the 9 directions with e_x = 0
-// are pulled with aligned float2 loads and all 19 outputs are written with
-// float2 stores, so every warp instruction moves 256 B like the fp64 sweep
+// Sweep with two cells per thread along x: the 9 directions with e_x = 0 are
+// pulled with aligned 2-vector loads (float2 / double2) and all 19 outputs are
+// written with 2-vector stores, so every fp32 warp instruction moves 256 B like
+// the one-cell fp64 sweep
 // (fp32 with one cell per thread sustains 5.45 TB/s of DRAM traffic vs 6.04 for
 // fp64, profiles/r01_ncu_*).  A pair containing a non-fluid cell stores
 // scalars: a wall cell's slots hold store-side bounce-back values of its
 // neighbours and must not be overwritten.  Block (32, 4) threads = 64 x 4 cells.
-template <int MINB, int STCS>
-__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<float> a)
+template <typename real> struct Vec2;
+template <> struct Vec2<float> { using T = float2; };
+template <> struct Vec2<double> { using T = double2; };
+
+template <typename real, int MINB, int STCS>
+__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)
 {
+    using V2 = typename Vec2<real>::T;
     const int64_t b = blockIdx.x;
     int lo = 0, hi = a.nboxes;
     while (hi - lo > 1) {
@@ -156,13 +162,13 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
     const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
     uint8_t k0 = a.kind[fbase];
     uint8_t k1 = has1 ? a.kind[fbase + 1] : (uint8_t)2;
-    const float *s = a.src + pbase;
-    float p0[Q], p1[Q];
+    const real *s = a.src + pbase;
+    real p0[Q], p1[Q];
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
         if (EX(i) == 0) {
-            const float2 v = __ldg(reinterpret_cast<const float2 *>(s + i * qs - sh));
+            const V2 v = __ldg(reinterpret_cast<const V2 *>(s + i * qs - sh));
             p0[i] = v.x;
             p1[i] = v.y;
         } else {
@@ -180,17 +186,27 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
             f1[j] = k1 == 1 ? a.flags[fbase + 1 + sh] : (uint8_t)0;
         }
     }
-    collide_bgk<float>(p0, a.omega);
-    collide_bgk<float>(p1, a.omega);
-    float *d = a.dst + pbase;
+    collide_bgk<real>(p0, a.omega);
+    collide_bgk<real>(p1, a.omega);
+    real *d = a.dst + pbase;
     if (k0 != 2 && k1 != 2) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            float2 *dp = reinterpret_cast<float2 *>(d + i * qs);
+            V2 *dp = reinterpret_cast<V2 *>(d + i * qs);
             if (STCS)
-                __stcs(dp, make_float2(p0[i], p1[i]));
+                {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                __stcs(dp, w);
+            }
             else
-                *dp = make_float2(p0[i], p1[i]);
+                {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *dp = w;
+            }
         }
     } else {
 #pragma unroll
@@ -205,7 +221,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
         for (int j = 1; j < Q; ++j)
             if (f0[j] != 0) {
                 const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-                float v = p0[j];
+                real v = p0[j];
                 if (f0[j] >= 2) v += a.corr[(f0[j] - 2) * Q + OPP(j)];
                 d[OPP(j) * qs + sh] = v;
             }
@@ -215,7 +231,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
         for (int j = 1; j < Q; ++j)
             if (f1[j] != 0) {
                 const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-                float v = p1[j];
+                real v = p1[j];
                 if (f1[j] >= 2) v += a.corr[(f1[j] - 2) * Q + OPP(j)];
                 d[OPP(j) * qs + sh + 1] = v;
             }
@@ -223,16 +239,16 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
 }
 
 template <typename real>
-static bool launch_x2(const SweepArgs<real> &, unsigned, int, cudaStream_t) { return false; }
-template <>
-bool launch_x2<float>(const SweepArgs<float> &a, unsigned grid, int variant, cudaStream_t s)
+static bool launch_x2(const SweepArgs<real> &a, unsigned grid, int variant, cudaStream_t s)
 {
     dim3 block(32, SWEEP_BY, 1);
+    // min blocks of 128 threads: fp32 4 / 5, fp64 2 / 3 (38 live doubles per thread)
+    constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
     switch (variant) {
-    case 12: sweep_x2_kernel<4, 0><<<grid, block, 0, s>>>(a); break;
-    case 13: sweep_x2_kernel<5, 0><<<grid, block, 0, s>>>(a); break;
-    case 14: sweep_x2_kernel<4, 1><<<grid, block, 0, s>>>(a); break;
-    default: sweep_x2_kernel<5, 1><<<grid, block, 0, s>>>(a); break;
+    case 12: sweep_x2_kernel<real, M0, 0><<<grid, block, 0, s>>>(a); break;
+    case 13: sweep_x2_kernel<real, M1, 0><<<grid, block, 0, s>>>(a); break;
+    case 14: sweep_x2_kernel<real, M0, 1><<<grid, block, 0, s>>>(a); break;
+    default: sweep_x2_kernel<real, M1, 1><<<grid, block, 0, s>>>(a); break;
     }
     return true;
 }
@@ -482,7 +498,7 @@ cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int vari
     case 9: sweep_kernel<real, 2, 1, 2><<<grid, block, 0, s>>>(a); break;
     case 10: sweep_kernel<real, 3, 0, 2><<<grid, block, 0, s>>>(a); break;
     case 11: sweep_kernel<real, 3, 1, 2><<<grid, block, 0, s>>>(a); break;
-    default: sweep_kernel<real, 3, 1, 1><<<grid, block, 0, s>>>(a); break;  // (x2 variants are fp32-only)
+    default: sweep_kernel<real, 3, 1, 1><<<grid, block, 0, s>>>(a); break;
     }
     return cudaGetLastError();
 }

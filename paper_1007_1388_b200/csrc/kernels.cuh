@@ -57,7 +57,7 @@ cudaError_t launch_wait_peers(const unsigned long long *inbox, const int *peer_r
                               const unsigned long long *epoch, int *error, cudaStream_t s);
 cudaError_t launch_signal_peers(unsigned long long *epoch, unsigned long long *const *peer_inbox, int npeers,
                                 cudaStream_t s);
-// variants 12..15 (fp32 only): two cells per thread along x, float2 accesses,
+// variants 12..15: two cells per thread along x, 2-vector accesses,
 // min blocks 4 / 5 of 128 threads, stcs 0 / 1.
 constexpr int kSweepVariants = 16;
 __host__ __device__ constexpr int sweep_cells_z(int variant) { return (variant >= 8 && variant < 12) ? 2 : 1; }

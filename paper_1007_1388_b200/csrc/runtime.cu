@@ -84,9 +84,9 @@ struct lbm_ctx {
     int device = 0;
     int align = kAlignDefault;
     // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
-    // fp32 two cells per thread with float2 accesses (x2), fp64 3 blocks/SM evict-first stores;
+    // two cells per thread with 2-vector accesses (x2): fp32 4 blocks/SM, fp64 3 blocks/SM (128 threads);
     // env LBM_SWEEP_VARIANT.
-    int sweep_variant[2] = {12, 5};
+    int sweep_variant[2] = {12, 13};
     int aa_variant[2] = {6, 2};
     int direct_variant[2] = {6, 5};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
     bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
@@ -1098,8 +1098,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {
         int v = std::atoi(a);
         if (v >= 0 && v < kSweepVariants) {
-            ctx->sweep_variant[0] = v;
-            if (v < 12) ctx->sweep_variant[1] = v;  // 12..15 exist for fp32 only
+            ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
         }
         if (v >= 0 && v < 8) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
         if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
