@@ -253,6 +253,155 @@ static bool launch_x2(const SweepArgs<real> &a, unsigned grid, int variant, cuda
     return true;
 }
 
+// AA-pattern kernels with two cells per thread along x (cf. sweep_x2_kernel):
+// LOCAL reads and writes only its own cells, so all 19 loads and 19 stores are
+// aligned 2-vectors; PULL vectorises the 9 gathers and scatters with e_x = 0.
+// A pair whose cells differ in kind (non-fluid, or a bounce-back redirect for
+// that direction) falls back to scalar accesses.
+template <typename real, bool PULL, int MINB>
+__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const SweepArgs<real> a)
+{
+    using V2 = typename Vec2<real>::T;
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    const int x0 = bx.lo[0] + tx * SWEEP_BX + 2 * (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    const int xend = bx.lo[0] + bx.n[0];
+    if (x0 >= xend || y >= bx.lo[1] + bx.n[1]) return;
+    const bool has1 = x0 + 1 < xend;
+
+    const Geom &g = a.g;
+    const int64_t qs = g.qs;
+    const int64_t cell = cell_index(g, x0, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k0 = a.kind[fbase];
+    const uint8_t k1 = has1 ? a.kind[fbase + 1] : (uint8_t)2;
+    real *A = a.dst + pbase;  // in place
+    real p0[Q], p1[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        if (PULL) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            const real *src = A + OPP(i) * qs - sh;
+            if (EX(i) == 0) {
+                const V2 v = __ldg(reinterpret_cast<const V2 *>(src));
+                p0[i] = v.x;
+                p1[i] = v.y;
+            } else {
+                p0[i] = __ldg(src);
+                p1[i] = __ldg(src + 1);
+            }
+        } else {
+            const V2 v = __ldg(reinterpret_cast<const V2 *>(A + i * qs));
+            p0[i] = v.x;
+            p1[i] = v.y;
+        }
+    }
+    if (k0 == 2 && k1 == 2) return;
+    uint8_t f0[Q], f1[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) f0[j] = f1[j] = 0;
+    if (k0 == 1 || k1 == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            if (k0 == 1) f0[j] = a.flags[fbase + sh];
+            if (k1 == 1) f1[j] = a.flags[fbase + 1 + sh];
+        }
+    }
+    collide_bgk<real>(p0, a.omega);
+    collide_bgk<real>(p1, a.omega);
+    const bool both = k0 != 2 && k1 != 2;
+    if (PULL) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            const bool r0 = f0[i] != 0, r1 = f1[i] != 0;  // x + e_i is a wall: bounce back into x
+            if (EX(i) == 0 && both && !r0 && !r1) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + i * qs + sh) = w;
+                continue;
+            }
+            if (k0 != 2) {
+                if (r0) {
+                    real v = p0[i];
+                    if (f0[i] >= 2) v += a.corr[(f0[i] - 2) * Q + OPP(i)];
+                    A[OPP(i) * qs] = v;
+                } else {
+                    A[i * qs + sh] = p0[i];
+                }
+            }
+            if (k1 != 2) {
+                if (r1) {
+                    real v = p1[i];
+                    if (f1[i] >= 2) v += a.corr[(f1[i] - 2) * Q + OPP(i)];
+                    A[OPP(i) * qs + 1] = v;
+                } else {
+                    A[i * qs + sh + 1] = p1[i];
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            if (both) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + OPP(i) * qs) = w;
+            } else {
+                if (k0 != 2) A[OPP(i) * qs] = p0[i];
+                if (k1 != 2) A[OPP(i) * qs + 1] = p1[i];
+            }
+        }
+        // store-side bounce-back into wall slots (see sweep_aa_kernel)
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            if (f0[j] != 0) {
+                real v = p0[j];
+                if (f0[j] >= 2) v += a.corr[(f0[j] - 2) * Q + OPP(j)];
+                A[j * qs + sh] = v;
+            }
+            if (f1[j] != 0) {
+                real v = p1[j];
+                if (f1[j] >= 2) v += a.corr[(f1[j] - 2) * Q + OPP(j)];
+                A[j * qs + sh + 1] = v;
+            }
+        }
+    }
+}
+
+template <typename real>
+static void launch_aa_x2(const SweepArgs<real> &a, unsigned grid, bool pull, int variant, cudaStream_t s)
+{
+    dim3 block(32, SWEEP_BY, 1);
+    constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
+    const bool m1 = variant == 13 || variant == 15;
+    if (pull) {
+        if (m1) sweep_aa_x2_kernel<real, true, M1><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, true, M0><<<grid, block, 0, s>>>(a);
+    } else {
+        if (m1) sweep_aa_x2_kernel<real, false, M1><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, false, M0><<<grid, block, 0, s>>>(a);
+    }
+}
+
 // 27 -> 18 neighbour-direction index (plan.cpp kDirs order; -1: centre / corner).
 __constant__ int8_t c_dir27[27] = {-1, 0,  -1, 1,  2,  3,  -1, 4,  -1, 5,  6,  7,  8, -1,
                                    9,  10, 11, 12, -1, 13, -1, 14, 15, 16, -1, 17, -1};
@@ -443,11 +592,18 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(cons
 }
 
 template <typename real>
+static void launch_aa_x2(const SweepArgs<real> &a, unsigned grid, bool pull, int variant, cudaStream_t s);
+
+template <typename real>
 cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s)
 {
     if (total_tiles <= 0) return cudaSuccess;
     dim3 block(SWEEP_BX, SWEEP_BY, 1);
     const unsigned grid = (unsigned)total_tiles;
+    if (variant >= 12) {
+        launch_aa_x2<real>(a, grid, pull, variant, s);
+        return cudaGetLastError();
+    }
     const int v = variant & 7;  // min blocks / store hint as for the two-grid sweep
     if (pull) {
         switch (v) {

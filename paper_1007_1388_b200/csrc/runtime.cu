@@ -87,7 +87,7 @@ struct lbm_ctx {
     // two cells per thread with 2-vector accesses (x2): fp32 4 blocks/SM, fp64 3 blocks/SM (128 threads);
     // env LBM_SWEEP_VARIANT.
     int sweep_variant[2] = {12, 13};
-    int aa_variant[2] = {6, 2};
+    int aa_variant[2] = {12, 13};  // AA kernels, two cells per thread (tools/sweep_tune.py --layout 1)
     int direct_variant[2] = {6, 5};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
     bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
     int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
@@ -1100,7 +1100,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if (v >= 0 && v < kSweepVariants) {
             ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
         }
-        if (v >= 0 && v < 8) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
+        if ((v >= 0 && v < 8) || v >= 12) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
         if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
     }
     if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
