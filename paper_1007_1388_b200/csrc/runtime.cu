@@ -216,7 +216,9 @@ Geom make_geom(const int n[3], int esize, int align)
     for (int a = 0; a < 3; ++a) g.n[a] = n[a];
     const int ae = align / esize;             // elements per alignment unit
     g.xo = ae;                                // x = -1 sits right before the aligned x = 0
-    g.px = ((g.xo + n[0] + 1 + ae - 1) / ae) * ae;
+    // columns up to x = n + 1 must exist: the two-cells-per-thread kernels read
+    // the phantom partner x0 + 1 = n of an odd row and its pull neighbour n + 1
+    g.px = ((g.xo + n[0] + 2 + ae - 1) / ae) * ae;
     g.py = n[1] + 2;
     g.plane = (int64_t)g.px * g.py;
     g.qs = g.plane * (n[2] + 2);

@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB)
     const int z = bx.lo[2] + tz;
     const Geom &g = a.g;
     const int64_t qs = g.qs;
-    bool remote_store = false;
 
     if (x < bx.lo[0] + bx.n[0] && y < bx.lo[1] + bx.n[1]) {
         const int64_t cell = cidx(g, x, y, z);
@@ -152,12 +151,10 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB)
 #pragma unroll
                     for (int q = 1; q < Q; ++q)
                         if (outgoing(q, kd)) nb[q * qs + gc] = p[q];
-                    if (dx.remote_mask[bx.patch] & (1u << kd)) remote_store = true;
                 }
             }
         }
     }
-    (void)remote_store;
 }
 
 // Publish this rank's step completion to its peers: runs after the sweep on the
