@@ -42,13 +42,8 @@ cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int vari
 // Sweep fused with the ghost exchange (sweep_direct.cu).
 template <typename real>
 struct DirectArgs {
-    real *const *nbr;                        // [nlocal][18][2]: neighbour patch base in grid i, or null
-    const uint32_t *remote_mask;             // [nlocal]: bit kd = neighbour kd lives on another GPU
-    int dsti;                                // destination grid index (0 / 1)
-    unsigned *cta_count;                     // completion counter, reset by the last CTA
-    unsigned long long *epoch;               // steps completed by this rank
-    unsigned long long *const *peer_inbox;   // [npeers]: &inbox_peer[my rank] (peer-mapped)
-    int npeers;
+    real *const *nbr;  // [nlocal][18][2]: remote neighbour patch base in (peer-mapped) grid i, or null
+    int dsti;          // destination grid index (0 / 1)
 };
 template <typename real>
 cudaError_t launch_sweep_direct(const SweepArgs<real> &a, const DirectArgs<real> &dx, int64_t total_tiles,

@@ -108,8 +108,6 @@ struct lbm_ctx {
     // into neighbour ghost layers (local or CUDA-IPC-mapped peer memory).
     bool direct = false;
     void **d_nbr = nullptr;                 // [nlocal][18][2] neighbour patch bases
-    uint32_t *d_remote_mask = nullptr;      // [nlocal]
-    unsigned *d_cta = nullptr;
     unsigned long long *d_epoch = nullptr;
     unsigned long long *d_inbox = nullptr;  // [nranks] epochs published by the peers
     unsigned long long **d_peer_inbox = nullptr;
@@ -746,12 +744,10 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         const DevBoxes &bs = ctx->box_shell;
         if (bs.tiles > 0) {
             if (ctx->esize == 8) {
-                DirectArgs<double> dx{(double *const *)ctx->d_nbr, ctx->d_remote_mask, dsti, ctx->d_cta,
-                                      ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct};
+                DirectArgs<double> dx{(double *const *)ctx->d_nbr, dsti};
                 e = launch_sweep_direct<double>(sweep_args<double>(ctx, bs), dx, bs.tiles, ctx->direct_variant[1], c);
             } else {
-                DirectArgs<float> dx{(float *const *)ctx->d_nbr, ctx->d_remote_mask, dsti, ctx->d_cta,
-                                     ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct};
+                DirectArgs<float> dx{(float *const *)ctx->d_nbr, dsti};
                 e = launch_sweep_direct<float>(sweep_args<float>(ctx, bs), dx, bs.tiles, ctx->direct_variant[0], c);
             }
             if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_direct launch", __LINE__);
@@ -942,8 +938,8 @@ void destroy_ctx(lbm_ctx *ctx)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_nbr, (void *)ctx->d_remote_mask, (void *)ctx->d_cta, (void *)ctx->d_epoch,
-                    (void *)ctx->d_inbox, (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
+    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
+                    (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
         if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)
         for (void *p : {(void *)X.pack_all.segs, (void *)X.pack_remote.segs, (void *)X.local_copy.segs,
@@ -973,11 +969,9 @@ lbm_status setup_direct(lbm_ctx *ctx)
     const Decomp &dec = ctx->dec;
     const int R = dec.nranks, me = dec.rank;
     lbm_status st;
-    if ((st = dev_alloc(ctx, &ctx->d_cta, sizeof(unsigned)))) return st;
     if ((st = dev_alloc(ctx, &ctx->d_epoch, sizeof(unsigned long long)))) return st;
     if ((st = dev_alloc(ctx, &ctx->d_inbox, (size_t)R * sizeof(unsigned long long)))) return st;
     if ((st = dev_alloc(ctx, &ctx->d_error, sizeof(int)))) return st;
-    CK(cudaMemset(ctx->d_cta, 0, sizeof(unsigned)));
     CK(cudaMemset(ctx->d_epoch, 0, sizeof(unsigned long long)));
     CK(cudaMemset(ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
     CK(cudaMemset(ctx->d_error, 0, sizeof(int)));
@@ -1033,7 +1027,6 @@ lbm_status setup_direct(lbm_ctx *ctx)
     // neighbour table
     const int nl = dec.nlocal;
     std::vector<void *> nbr((size_t)nl * NDIR * 2, nullptr);
-    std::vector<uint32_t> rmask(nl, 0);
     for (int l = 0; l < nl; ++l) {
         const int gpatch = dec.local_to_global(l);
         for (int k = 0; k < NDIR; ++k) {
@@ -1046,13 +1039,10 @@ lbm_status setup_direct(lbm_ctx *ctx)
                 char *base = (char *)peer_grid[(size_t)2 * r + i];
                 nbr[((size_t)l * NDIR + k) * 2 + i] = base + off;
             }
-            rmask[l] |= 1u << k;
         }
     }
     if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
     CK(cudaMemcpy(ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *), cudaMemcpyHostToDevice));
-    if ((st = dev_alloc(ctx, &ctx->d_remote_mask, rmask.size() * sizeof(uint32_t)))) return st;
-    CK(cudaMemcpy(ctx->d_remote_mask, rmask.data(), rmask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     std::vector<unsigned long long *> pin;
     std::vector<int> prank;
     for (int r : peers) {

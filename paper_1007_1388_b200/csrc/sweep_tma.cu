@@ -334,13 +334,10 @@ static cudaError_t launch_v(const CUtensorMap &pm, const CUtensorMap &km, const 
     constexpr int TX = TmaShape<real, V>::TX, TY = TmaShape<real, V>::TY, ST = TmaShape<real, V>::ST;
     constexpr int CPS = TmaShape<real, V>::CPS;
     using C = TmaCfg<real, TX, TY, ST, CPS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(sweep_tma_kernel<real, TX, TY, ST, CPS>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    // per launch (cheap, and correct for whichever device is current)
+    cudaError_t e = cudaFuncSetAttribute(sweep_tma_kernel<real, TX, TY, ST, CPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * CPS;
     if (grid > total_tiles) grid = total_tiles;
     sweep_tma_kernel<real, TX, TY, ST, CPS><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(pm, km, fm, a, total_tiles);
