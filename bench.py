@@ -340,10 +340,13 @@ def main():
         barrier()
         t0 = time.perf_counter()
         L.set_pdfs(host_f)
+        t1 = time.perf_counter()
         L.step(args.steps)
+        t2 = time.perf_counter()
         L.get_macroscopic(host_rho, host_u)
         barrier()
         e2e_s = time.perf_counter() - t0
+        e2e_parts = {"set_pdfs_s": t1 - t0, "steps_s": t2 - t1, "get_macroscopic_s": time.perf_counter() - t2}
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -351,7 +354,7 @@ def main():
         e2e = {"value": fluid_global * args.steps / e2e_s / 1e6, "unit": "MFLUPS",
                "h2d_bytes_per_step": host_f.nbytes * world / args.steps,
                "d2h_bytes_per_step": (host_rho.nbytes + host_u.nbytes) * world / args.steps,
-               "job": "set_pdfs(host state) + lbm_step(K) + get_macroscopic(host)"}
+               "job": "set_pdfs(host state) + lbm_step(K) + get_macroscopic(host)", "rank0_parts": e2e_parts}
         del host_f, host_rho, host_u
 
     # ---- cpu baseline (rank 0, N = 1 only)

@@ -1,0 +1,104 @@
+// stream_ceiling.cu -- bandwidth ceiling of the sweep's access pattern on this GPU.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o build/stream_ceiling tools/stream_ceiling.cu
+//   build/stream_ceiling [n=256] [elem=8]
+// Streams 19 q-slices in and 19 out over an n^3 lattice with the sweep's
+// padded layout (row pitch roundup(xo + n + 2, 128 B)), two cells per thread,
+// no arithmetic: (a) aligned copy, (b) pull-shifted reads (x - e_i per slice).
+// Reports algorithmic GB/s = 2 * 19 * elem * n^3 / time.  Also a plain 1-D copy.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+constexpr int Q = 19;
+__constant__ int cEX[Q] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
+__constant__ int cEY[Q] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
+__constant__ int cEZ[Q] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+
+template <typename T, bool SHIFT>
+__global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ src, T *__restrict__ dst, int n,
+                                                        int px, long long plane, long long qs, int xo)
+{
+    const int x0 = blockIdx.x * 64 + 2 * threadIdx.x;
+    const int y = blockIdx.y * 4 + threadIdx.y;
+    const int z = blockIdx.z;
+    if (x0 >= n || y >= n) return;
+    const long long cell = ((long long)(z + 1) * (n + 2) + (y + 1)) * px + x0 + xo;
+    T a[Q], b[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const long long sh = SHIFT ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
+        a[i] = __ldg(src + cell + i * qs - sh);
+        b[i] = __ldg(src + cell + i * qs - sh + 1);
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        dst[cell + i * qs] = a[i];
+        dst[cell + i * qs + 1] = b[i];
+    }
+}
+
+template <typename T>
+__global__ void copy1d(const T *__restrict__ s, T *__restrict__ d, long long n)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+template <typename T>
+void run(int n)
+{
+    const int ae = 128 / sizeof(T), xo = ae;
+    const int px = ((xo + n + 2 + ae - 1) / ae) * ae;
+    const long long plane = (long long)px * (n + 2), qs = plane * (n + 2);
+    const size_t bytes = (size_t)Q * qs * sizeof(T);
+    T *a, *b;
+    cudaMalloc(&a, bytes);
+    cudaMalloc(&b, bytes);
+    cudaMemset(a, 0, bytes);
+    cudaMemset(b, 0, bytes);
+    dim3 grid((n + 63) / 64, (n + 3) / 4, n), block(32, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n;
+    for (int shift = 0; shift < 2; ++shift) {
+        for (int w = 0; w < 5; ++w)
+            shift ? stream_kernel<T, true><<<grid, block>>>(a, b, n, px, plane, qs, xo)
+                  : stream_kernel<T, false><<<grid, block>>>(a, b, n, px, plane, qs, xo);
+        const int reps = 50;
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r) {
+            if (shift)
+                stream_kernel<T, true><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
+            else
+                stream_kernel<T, false><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
+        }
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("elem=%zu n=%d %s: %.3f ms/launch, %.1f GB/s algorithmic\n", sizeof(T), n,
+               shift ? "pull-shifted 19-in/19-out" : "aligned 19-in/19-out", ms / reps, alg / (ms / reps * 1e-3) / 1e9);
+    }
+    const long long ne = (long long)(bytes / sizeof(T));
+    for (int w = 0; w < 3; ++w) copy1d<T><<<148 * 8, 256>>>(a, b, ne);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; ++r) copy1d<T><<<148 * 8, 256>>>(r & 1 ? b : a, r & 1 ? a : b, ne);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("elem=%zu plain 1-D copy of %.2f GB: %.1f GB/s (read+write)\n", sizeof(T), bytes / 1e9,
+           2.0 * bytes / (ms / 20 * 1e-3) / 1e9);
+    cudaFree(a);
+    cudaFree(b);
+}
+
+int main(int argc, char **argv)
+{
+    const int n = argc > 1 ? atoi(argv[1]) : 256;
+    run<double>(n);
+    run<float>(n);
+    return 0;
+}
