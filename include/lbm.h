@@ -153,6 +153,9 @@ typedef struct {
                                               0: pack -> NCCL / copy -> unpack             */
     int32_t local_pull;                    /* 1: face cells read same-GPU neighbour patches
                                               directly (no ghost copies between them)      */
+    int32_t local_direct;                  /* 1: the sweep stores the outgoing PDFs of face /
+                                              edge cells straight into same-GPU neighbour
+                                              patches' ghost layers (no ghost copies)     */
 } lbm_info;
 
 /* One remote message of the static exchange plan (lbm_plan, host-only).      */

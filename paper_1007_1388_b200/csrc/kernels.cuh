@@ -31,7 +31,30 @@ struct SweepArgs {
     // of from a ghost copy.  lnbr == nullptr disables it.
     const real *const *lnbr = nullptr;
     int srci = 0;
+    // Direct ghost stores (x2 sweep): [nlocal][18][2] base of the neighbour patch
+    // (same GPU, or peer-mapped) in grid i, null where the copy path serves it.
+    // Face / edge cells store their outgoing PDFs into that patch's ghost cell
+    // of grid dsti.  dnbr == nullptr disables it.
+    real *const *dnbr = nullptr;
+    int dsti = 0;
 };
+
+// The 18 neighbour directions in the plan's order (plan.cpp kDirs).
+__host__ __device__ constexpr int ndir(int k, int a)
+{
+    constexpr int t[NDIR][3] = {{0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {1, 0, -1}, {0, 1, -1}, {-1, -1, 0},
+                                {0, -1, 0},  {1, -1, 0},  {-1, 0, 0}, {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},
+                                {1, 1, 0},   {0, -1, 1},  {-1, 0, 1}, {0, 0, 1},  {1, 0, 1},  {0, 1, 1}};
+    return t[k][a];
+}
+
+// Does direction q travel into the neighbour at d (e_q[a] == d[a] on every
+// axis where d is non-zero)?  5 q per face, 1 per edge.
+__host__ __device__ constexpr bool outgoing(int q, int k)
+{
+    return q != 0 && (ndir(k, 0) == 0 || EXf(q) == ndir(k, 0)) && (ndir(k, 1) == 0 || EYf(q) == ndir(k, 1)) &&
+           (ndir(k, 2) == 0 || EZf(q) == ndir(k, 2));
+}
 
 // variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first stores,
 // one cell per thread; variants 8..11: two cells per thread along z (tiles span

@@ -125,6 +125,10 @@ struct lbm_ctx {
     // no ghost copies between local patches.
     bool lpull = false;
     void **d_lnbr = nullptr;                // [nlocal][18][2]
+    // direct ghost stores by the x2 sweep (same-GPU and, with `direct`, peer patches)
+    bool ldirect = false;
+    void **d_dnbr = nullptr;                // [nlocal][18][2]
+    std::vector<void *> h_nbr;              // setup_direct's peer-mapped table
     int layout = LBM_LAYOUT_AB;
     int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
     void *sendbuf = nullptr, *recvbuf = nullptr;
@@ -554,6 +558,8 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.nboxes = b.n;
     a.lnbr = ctx->lpull ? (const real *const *)ctx->d_lnbr : nullptr;
     a.srci = ctx->cur;
+    a.dnbr = ctx->ldirect && ctx->layout == LBM_LAYOUT_AB ? (real *const *)ctx->d_dnbr : nullptr;
+    a.dsti = 1 - ctx->cur;
     return a;
 }
 
@@ -622,17 +628,20 @@ lbm_status transport(lbm_ctx *ctx, const ExSet &X, cudaStream_t s)
 }
 
 // Ghost refresh of grid `gi` (used after set_pdfs / init and inside the step).
-lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, int kind)
+// in_step: right after a sweep, whose direct stores (ldirect) already filled
+// the same-GPU ghosts.
+lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, int kind, bool in_step)
 {
     void *grid = ctx->grid[gi];
     const ExSet &X = ctx->ex[kind];
     lbm_status st;
-    const bool work = (ctx->lpull ? X.pack_remote.n : X.pack_all.n) > 0 || X.has_remote || X.unpack.n > 0;
+    // local pull: same-GPU neighbours are read in place, only remote segments move
+    const bool skip_local = ctx->lpull || (in_step && ctx->ldirect);
+    const bool work = (skip_local ? X.pack_remote.n : X.pack_all.n) > 0 || X.has_remote || X.unpack.n > 0;
     if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
     if (ts) ts->exchange = true;
     if (ts) CK(cudaEventRecord(ts->ev[2], s));
-    // local pull: same-GPU neighbours are read in place, only remote segments move
-    if ((st = launch_copy(ctx, ctx->lpull ? X.pack_remote : X.pack_all, grid, grid, nullptr, ctx->sendbuf, s)))
+    if ((st = launch_copy(ctx, skip_local ? X.pack_remote : X.pack_all, grid, grid, nullptr, ctx->sendbuf, s)))
         return st;
     if (ts) CK(cudaEventRecord(ts->ev[3], s));
     if (X.has_remote) {
@@ -651,7 +660,7 @@ lbm_status refresh_state(lbm_ctx *ctx)
     // AB: ghost layers of the current grid.  AA (swapped state): half-exchange 1,
     // which is what the next PULL step gathers from the ghost layers.
     const bool aa = ctx->layout == LBM_LAYOUT_AA;
-    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB);
+    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB, false);
     if (st) return st;
     cudaError_t e = ctx->esize == 8
                         ? launch_bb_fill<double>((double *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
@@ -749,11 +758,12 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         ctx->launches += 1;
         const DevBoxes &bs = ctx->box_shell;
         if (bs.tiles > 0) {
+            void **tab = ctx->ldirect ? ctx->d_dnbr : ctx->d_nbr;
             if (ctx->esize == 8) {
-                DirectArgs<double> dx{(double *const *)ctx->d_nbr, dsti};
+                DirectArgs<double> dx{(double *const *)tab, dsti};
                 e = launch_sweep_direct<double>(sweep_args<double>(ctx, bs), dx, bs.tiles, ctx->direct_variant[1], c);
             } else {
-                DirectArgs<float> dx{(float *const *)ctx->d_nbr, dsti};
+                DirectArgs<float> dx{(float *const *)tab, dsti};
                 e = launch_sweep_direct<float>(sweep_args<float>(ctx, bs), dx, bs.tiles, ctx->direct_variant[0], c);
             }
             if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_direct launch", __LINE__);
@@ -765,10 +775,10 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ev_shell, c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         CK(cudaStreamWaitEvent(s, ev_shell, 0));
-        if ((st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
+        if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
     } else if (!ctx->use_overlap) {
         if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
-        if ((st = exchange_seq(ctx, dsti, s, ts, kind))) return st;
+        if ((st = exchange_seq(ctx, dsti, s, ts, kind, true))) return st;
     } else {
         cudaStream_t c = ctx->comm_stream;
         // S: shells facing remote neighbours, then pack them.
@@ -787,7 +797,8 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
-        if (!ctx->lpull && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
+        if (!ctx->lpull && !ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
+            return st;
         CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
     }
     if (ts) CK(cudaEventRecord(ts->ev[kEvPerSlot - 1], s));
@@ -944,7 +955,7 @@ void destroy_ctx(lbm_ctx *ctx)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
+    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_dnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
                     (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
         if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)
@@ -1053,6 +1064,7 @@ lbm_status setup_direct(lbm_ctx *ctx)
             }
         }
     }
+    ctx->h_nbr = nbr;
     if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
     CK(cudaMemcpy(ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *), cudaMemcpyHostToDevice));
     std::vector<unsigned long long *> pin;
@@ -1282,6 +1294,34 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
                 cudaSuccess)
                 return bail(LBM_ERR_CUDA);
             ctx->lpull = true;
+        }
+    }
+    {
+        // Direct ghost stores for same-GPU neighbours (two-grid x2 sweep): the sweep
+        // writes the outgoing PDFs of face / edge cells straight into the neighbour
+        // patches' ghost layers, replacing the ghost copies after the sweep.  Default
+        // on; LBM_LOCAL_DIRECT=0 keeps the copies.
+        const char *ev = std::getenv("LBM_LOCAL_DIRECT");
+        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
+        const bool want = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && !ctx->lpull &&
+                          cfg->exchange_mode == LBM_EXCHANGE_AUTO && v >= 12 && !(ev && std::string(ev) == "0") &&
+                          !ctx->ex[EX_AB].segs.local.empty();
+        if (want) {
+            std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);
+            for (int l = 0; l < dec.nlocal; ++l) {
+                const int gp = dec.local_to_global(l);
+                for (int k = 0; k < NDIR; ++k) {
+                    const int nbp = neighbour(dec, gp, kDirs[k].d);
+                    if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
+                    const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
+                }
+            }
+            if ((st = dev_alloc(ctx, &ctx->d_dnbr, tab.size() * sizeof(void *)))) return bail(st);
+            if (cudaMemcpy(ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+                return bail(LBM_ERR_CUDA);
+            ctx->ldirect = true;
         }
     }
     // Default geometry: closed no-slip box at rest (f~ = 0).
@@ -1676,6 +1716,7 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
     out->aa_phase = ctx->aa_phase;
     out->exchange_fused = ctx->direct ? 1 : 0;
     out->local_pull = ctx->lpull ? 1 : 0;
+    out->local_direct = ctx->ldirect ? 1 : 0;
     if (ctx->lpull) out->halo_bytes_local_per_step = 0;
     return LBM_OK;
 }

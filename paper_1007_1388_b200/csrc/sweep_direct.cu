@@ -37,23 +37,6 @@ __device__ __forceinline__ int64_t cidx(const Geom &g, int x, int y, int z)
     return ((int64_t)(z + 1) * g.py + (y + 1)) * (int64_t)g.px + (x + g.xo);
 }
 
-// The 18 neighbour directions in the plan's order (plan.cpp kDirs).
-__host__ __device__ constexpr int ndir(int k, int a)
-{
-    constexpr int t[NDIR][3] = {{0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {1, 0, -1}, {0, 1, -1}, {-1, -1, 0},
-                                {0, -1, 0},  {1, -1, 0},  {-1, 0, 0}, {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},
-                                {1, 1, 0},   {0, -1, 1},  {-1, 0, 1}, {0, 0, 1},  {1, 0, 1},  {0, 1, 1}};
-    return t[k][a];
-}
-
-// Does direction q travel into the neighbour at d (e_q[a] == d[a] on every
-// axis where d is non-zero)?  5 q per face, 1 per edge.
-__host__ __device__ constexpr bool outgoing(int q, int k)
-{
-    return q != 0 && (ndir(k, 0) == 0 || EXf(q) == ndir(k, 0)) && (ndir(k, 1) == 0 || EYf(q) == ndir(k, 1)) &&
-           (ndir(k, 2) == 0 || EZf(q) == ndir(k, 2));
-}
-
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v)
 {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -56,7 +56,7 @@ class LbmInfo(ctypes.Structure):
                 ("phase_count", ctypes.c_int64 * NPHASES), ("row_pitch_elems", ctypes.c_int64),
                 ("align_bytes", ctypes.c_int32), ("graphs_active", ctypes.c_int32), ("layout", ctypes.c_int32),
                 ("aa_phase", ctypes.c_int32), ("exchange_fused", ctypes.c_int32),
-                ("local_pull", ctypes.c_int32)]
+                ("local_pull", ctypes.c_int32), ("local_direct", ctypes.c_int32)]
 
     def to_dict(self) -> dict:
         out = {}

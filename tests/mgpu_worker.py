@@ -33,7 +33,10 @@ def main():
     # by default; "nccl" forces pack -> NCCL -> unpack (LBM_EXCHANGE=nccl)
     # plus process grids that split x (the driver's 8-GPU run is 2x2x2)
     grids = {2: [(0, 0, 0), (2, 1, 1)], 4: [(0, 0, 0), (2, 2, 1), (2, 1, 2)]}.get(world, [(0, 0, 0)])
-    combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "nccl", grids[0]),
+    # "fused_copies": fused exchange with same-GPU ghost copies instead of the
+    # sweep's direct ghost stores (LBM_LOCAL_DIRECT=0)
+    combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "fused_copies", grids[0]),
+              (8, 1, 0, "nccl", grids[0]),
               (8, 0, 0, "nccl", grids[0]), (4, 1, 0, "nccl", grids[0]), (8, 1, 1, "nccl", grids[0]),
               (4, 0, 1, "nccl", grids[0])]
     for pg in grids[1:]:
@@ -43,6 +46,10 @@ def main():
             os.environ["LBM_EXCHANGE"] = "nccl"
         else:
             os.environ.pop("LBM_EXCHANGE", None)
+        if exch == "fused_copies":
+            os.environ["LBM_LOCAL_DIRECT"] = "0"
+        else:
+            os.environ.pop("LBM_LOCAL_DIRECT", None)
         if True:
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -62,9 +69,11 @@ def main():
                 for lo, hi, a in parts:
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
                 results[(prec, overlap, layout, exch, tuple(pgrid))] = full
-                assert info["exchange_fused"] == (1 if exch == "fused" else 0), info["exchange_fused"]
+                assert info["exchange_fused"] == (1 if exch.startswith("fused") else 0), info["exchange_fused"]
+                # 8+ patches per rank: same-GPU neighbours take the direct ghost stores (AB)
+                assert info["local_direct"] == (1 if layout == 0 and exch != "fused_copies" else 0), info
                 print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} peers={info['peers']} "
-                      f"halo={info['halo_bytes_remote_per_step']}", flush=True)
+                      f"halo={info['halo_bytes_remote_per_step']} local_direct={info['local_direct']}", flush=True)
     if rank == 0:
         import oracle
         ref = oracle.run(inputs.noise_pdfs(domain), fl, wu, inputs.LDC_OMEGA, steps, periodic=periodic,

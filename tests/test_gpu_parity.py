@@ -281,3 +281,32 @@ def test_local_pull_equals_ghost_copies(prec, monkeypatch):
     np.testing.assert_array_equal(out["1"], out["0"])
     one = run_gpu(n, fl, wu, f0, 11, prec, periodic=(1, 0, 1))
     np.testing.assert_array_equal(out["1"], one)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("n,patch,periodic", [((64, 30, 24), (16, 10, 12), (1, 0, 1)),
+                                              ((60, 30, 24), (15, 30, 8), (1, 1, 0))])
+def test_local_direct_equals_ghost_copies(prec, n, patch, periodic, monkeypatch):
+    """The x2 sweep storing face / edge PDFs straight into same-GPU neighbour
+    ghosts (the default) gives bitwise the ghost-copy result and the one-patch
+    result: obstacles on patch boundaries, two moving walls, odd patch widths,
+    a periodic self-neighbour (one patch along periodic y)."""
+    fl, wu = inputs.ldc_flags(n, periodic=periodic)
+    fl = inputs.add_obstacles(fl, 0.06, seed=31, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.0, 0.01, 0.02]]])
+    f0 = inputs.noise_pdfs(n, seed=37)
+    out = {}
+    for ld in ("1", "0"):
+        monkeypatch.setenv("LBM_LOCAL_DIRECT", ld)
+        L = lbm().Lattice(n, patch, inputs.LDC_OMEGA, prec, periodic=periodic)
+        assert L.info()["local_direct"] == int(ld)
+        L.set_flags(fl, wu)
+        L.set_pdfs(f0)
+        L.step(11)
+        out[ld] = L.get_pdfs()
+        L.close()
+    np.testing.assert_array_equal(out["1"], out["0"])
+    one = run_gpu(n, fl, wu, f0, 11, prec, periodic=periodic)
+    np.testing.assert_array_equal(out["1"], one)
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 11, periodic=periodic, nthreads=oracle.max_threads())
+    assert max_fluid_diff(out["1"], ref, fl) <= TOL[prec]

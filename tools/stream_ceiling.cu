@@ -1,6 +1,8 @@
 // stream_ceiling.cu -- bandwidth ceiling of the sweep's access pattern on this GPU.
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o build/stream_ceiling tools/stream_ceiling.cu
-//   build/stream_ceiling [n=256] [elem=8]
+//   build/stream_ceiling [n=256] [patches=1]
+// patches > 1: that many n^3 patches, each with its own ghost shell (the
+// patch-heavy layout), z of the grid running over patch * n + z.
 // Streams 19 q-slices in and 19 out over an n^3 lattice with the sweep's
 // padded layout (row pitch roundup(xo + n + 2, 128 B)), two cells per thread,
 // no arithmetic: (a) aligned copy, (b) pull-shifted reads (x - e_i per slice).
@@ -21,9 +23,10 @@ __global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ sr
 {
     const int x0 = blockIdx.x * 64 + 2 * threadIdx.x;
     const int y = blockIdx.y * 4 + threadIdx.y;
-    const int z = blockIdx.z;
+    const int z = blockIdx.z % n;
+    const long long pbase = (long long)(blockIdx.z / n) * Q * qs;
     if (x0 >= n || y >= n) return;
-    const long long cell = ((long long)(z + 1) * (n + 2) + (y + 1)) * px + x0 + xo;
+    const long long cell = pbase + ((long long)(z + 1) * (n + 2) + (y + 1)) * px + x0 + xo;
     T a[Q], b[Q];
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
@@ -46,22 +49,22 @@ __global__ void copy1d(const T *__restrict__ s, T *__restrict__ d, long long n)
 }
 
 template <typename T>
-void run(int n)
+void run(int n, int P)
 {
     const int ae = 128 / sizeof(T), xo = ae;
     const int px = ((xo + n + 2 + ae - 1) / ae) * ae;
     const long long plane = (long long)px * (n + 2), qs = plane * (n + 2);
-    const size_t bytes = (size_t)Q * qs * sizeof(T);
+    const size_t bytes = (size_t)P * Q * qs * sizeof(T);
     T *a, *b;
     cudaMalloc(&a, bytes);
     cudaMalloc(&b, bytes);
     cudaMemset(a, 0, bytes);
     cudaMemset(b, 0, bytes);
-    dim3 grid((n + 63) / 64, (n + 3) / 4, n), block(32, 4);
+    dim3 grid((n + 63) / 64, (n + 3) / 4, n * P), block(32, 4);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n;
+    const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n * P;
     for (int shift = 0; shift < 2; ++shift) {
         for (int w = 0; w < 5; ++w)
             shift ? stream_kernel<T, true><<<grid, block>>>(a, b, n, px, plane, qs, xo)
@@ -78,7 +81,7 @@ void run(int n)
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        printf("elem=%zu n=%d %s: %.3f ms/launch, %.1f GB/s algorithmic\n", sizeof(T), n,
+        printf("elem=%zu n=%d patches=%d %s: %.3f ms/launch, %.1f GB/s algorithmic\n", sizeof(T), n, P,
                shift ? "pull-shifted 19-in/19-out" : "aligned 19-in/19-out", ms / reps, alg / (ms / reps * 1e-3) / 1e9);
     }
     const long long ne = (long long)(bytes / sizeof(T));
@@ -98,7 +101,8 @@ void run(int n)
 int main(int argc, char **argv)
 {
     const int n = argc > 1 ? atoi(argv[1]) : 256;
-    run<double>(n);
-    run<float>(n);
+    const int P = argc > 2 ? atoi(argv[2]) : 1;
+    run<double>(n, P);
+    run<float>(n, P);
     return 0;
 }
