@@ -403,7 +403,13 @@ static bool launch_x2(const SweepArgs<real> &a, unsigned grid, int variant, cuda
 // LOCAL reads and writes only its own cells, so all 19 loads and 19 stores are
 // aligned 2-vectors; PULL vectorises the 9 gathers and scatters with e_x = 0.
 // A pair whose cells differ in kind (non-fluid, or a bounce-back redirect for
-// that direction) falls back to scalar accesses.
+// that direction) falls back to scalar accesses.  Pairs with no wall next to
+// either cell (kind 0, the common case) take a straight-line store path: the
+// per-direction redirect tests cost PULL +41 % instructions over the two-grid
+// sweep in this latency-bound kernel (1.05 -> 0.88 ms at 256^3 fp64,
+// profiles/r01_ncu_aa_*).  Realigning the 10 e_x != 0 scatters into 2-vectors
+// with warp shuffles was measured slower (tools/stream_ceiling.cu mode 3: the
+// ceiling gains 1.6 %, the kernel loses more to the shuffles).
 template <typename real, bool PULL, int MINB>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const SweepArgs<real> a)
 {
@@ -471,7 +477,22 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     collide_bgk<real>(p0, a.omega);
     collide_bgk<real>(p1, a.omega);
     const bool both = k0 != 2 && k1 != 2;
-    if (PULL) {
+    if (PULL && k0 == 0 && k1 == 0) {
+        // no wall next to either cell (the common case): straight-line scatter
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            if (EX(i) == 0) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + i * qs + sh) = w;
+            } else {
+                A[i * qs + sh] = p0[i];
+                A[i * qs + sh + 1] = p1[i];
+            }
+        }
+    } else if (PULL) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
@@ -503,18 +524,22 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
             }
         }
     } else {
+        if (both) {
 #pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            if (both) {
+            for (int i = 0; i < Q; ++i) {
                 V2 w;
                 w.x = p0[i];
                 w.y = p1[i];
                 *reinterpret_cast<V2 *>(A + OPP(i) * qs) = w;
-            } else {
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
                 if (k0 != 2) A[OPP(i) * qs] = p0[i];
                 if (k1 != 2) A[OPP(i) * qs + 1] = p1[i];
             }
         }
+        if (k0 != 1 && k1 != 1) return;
         // store-side bounce-back into wall slots (see sweep_aa_kernel)
 #pragma unroll
         for (int j = 1; j < Q; ++j) {
@@ -538,6 +563,7 @@ static void launch_aa_x2(const SweepArgs<real> &a, unsigned grid, bool pull, int
 {
     dim3 block(32, SWEEP_BY, 1);
     constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
+    // 12 / 14: min blocks M0; 13 / 15: M1
     const bool m1 = variant == 13 || variant == 15;
     if (pull) {
         if (m1) sweep_aa_x2_kernel<real, true, M1><<<grid, block, 0, s>>>(a);

@@ -11,13 +11,17 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 constexpr int Q = 19;
 __constant__ int cEX[Q] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
 __constant__ int cEY[Q] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
 __constant__ int cEZ[Q] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
 
-template <typename T, bool SHIFT>
+// SHIFT 0: aligned; 1: pull-shifted reads (x - e_i); 2: pull-shifted reads and
+// push-shifted writes (x + e_i, the AA PULL step's scatter); 3: as 2, but the
+// e_x != 0 scatters realigned through warp shuffles into 2-vector stores.
+template <typename T, int SHIFT>
 __global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ src, T *__restrict__ dst, int n,
                                                         int px, long long plane, long long qs, int xo)
 {
@@ -36,8 +40,36 @@ __global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ sr
     }
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
-        dst[cell + i * qs] = a[i];
-        dst[cell + i * qs + 1] = b[i];
+        const long long sh = SHIFT >= 2 ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
+        if (SHIFT == 3 && cEX[i] != 0) {
+            // pair (x0, x0 + 1) of the destination row: e_x = +1 -> (b of lane - 1, a);
+            // e_x = -1 -> (b, a of lane + 1); edge lanes store their stray element alone
+            const int lane = threadIdx.x;
+            using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
+            T *row = dst + cell + i * qs + (sh - cEX[i]);
+            if (cEX[i] > 0) {
+                const T up = __shfl_up_sync(0xffffffffu, b[i], 1);
+                if (lane > 0) {
+                    V2 w; w.x = up; w.y = a[i];
+                    *reinterpret_cast<V2 *>(row) = w;
+                } else {
+                    row[1] = a[i];
+                }
+                if (lane == 31) row[2] = b[i];
+            } else {
+                const T dn = __shfl_down_sync(0xffffffffu, a[i], 1);
+                if (lane < 31) {
+                    V2 w; w.x = b[i]; w.y = dn;
+                    *reinterpret_cast<V2 *>(row) = w;
+                } else {
+                    row[0] = b[i];
+                }
+                if (lane == 0) row[-1] = a[i];
+            }
+        } else {
+            dst[cell + i * qs + sh] = a[i];
+            dst[cell + i * qs + sh + 1] = b[i];
+        }
     }
 }
 
@@ -65,24 +97,27 @@ void run(int n, int P)
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n * P;
-    for (int shift = 0; shift < 2; ++shift) {
-        for (int w = 0; w < 5; ++w)
-            shift ? stream_kernel<T, true><<<grid, block>>>(a, b, n, px, plane, qs, xo)
-                  : stream_kernel<T, false><<<grid, block>>>(a, b, n, px, plane, qs, xo);
+    auto launch = [&](int shift, T *s, T *d) {
+        switch (shift) {
+        case 0: stream_kernel<T, 0><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        case 1: stream_kernel<T, 1><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        case 2: stream_kernel<T, 2><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        default: stream_kernel<T, 3><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        }
+    };
+    const char *names[4] = {"aligned 19-in/19-out", "pull-shifted 19-in/19-out", "pull reads + push-shifted writes",
+                            "pull reads + push writes, shuffle-aligned"};
+    for (int shift = 0; shift < 4; ++shift) {
+        for (int w = 0; w < 5; ++w) launch(shift, a, b);
         const int reps = 50;
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) {
-            if (shift)
-                stream_kernel<T, true><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
-            else
-                stream_kernel<T, false><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
-        }
+        for (int r = 0; r < reps; ++r) launch(shift, r & 1 ? b : a, r & 1 ? a : b);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         printf("elem=%zu n=%d patches=%d %s: %.3f ms/launch, %.1f GB/s algorithmic\n", sizeof(T), n, P,
-               shift ? "pull-shifted 19-in/19-out" : "aligned 19-in/19-out", ms / reps, alg / (ms / reps * 1e-3) / 1e9);
+               names[shift], ms / reps, alg / (ms / reps * 1e-3) / 1e9);
     }
     const long long ne = (long long)(bytes / sizeof(T));
     for (int w = 0; w < 3; ++w) copy1d<T><<<148 * 8, 256>>>(a, b, ne);
