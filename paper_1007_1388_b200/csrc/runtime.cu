@@ -126,7 +126,8 @@ struct lbm_ctx {
     bool lpull = false;
     void **d_lnbr = nullptr;                // [nlocal][18][2]
     // direct ghost stores by the x2 sweep (same-GPU and, with `direct`, peer patches)
-    bool ldirect = false;
+    bool ldirect = false;                   // same-GPU neighbours: no ghost copies
+    bool x2_shells = false;                 // fused exchange: shells swept by the x2 kernel
     void **d_dnbr = nullptr;                // [nlocal][18][2]
     std::vector<void *> h_nbr;              // setup_direct's peer-mapped table
     int layout = LBM_LAYOUT_AB;
@@ -757,7 +758,19 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         if (e != cudaSuccess) return ctx->cuda_fail(e, "wait_peers launch", __LINE__);
         ctx->launches += 1;
         const DevBoxes &bs = ctx->box_shell;
-        if (bs.tiles > 0) {
+        if (bs.tiles > 0 && ctx->x2_shells) {
+            if (ctx->esize == 8) {
+                SweepArgs<double> a = sweep_args<double>(ctx, bs);
+                a.dnbr = (double *const *)ctx->d_dnbr;
+                e = launch_sweep<double>(a, bs.tiles, ctx->sweep_variant[1], c);
+            } else {
+                SweepArgs<float> a = sweep_args<float>(ctx, bs);
+                a.dnbr = (float *const *)ctx->d_dnbr;
+                e = launch_sweep<float>(a, bs.tiles, ctx->sweep_variant[0], c);
+            }
+            if (e != cudaSuccess) return ctx->cuda_fail(e, "shell sweep launch", __LINE__);
+            ctx->launches += 1;
+        } else if (bs.tiles > 0) {
             void **tab = ctx->ldirect ? ctx->d_dnbr : ctx->d_nbr;
             if (ctx->esize == 8) {
                 DirectArgs<double> dx{(double *const *)tab, dsti};
@@ -1301,18 +1314,24 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         }
     }
     {
-        // Direct ghost stores for same-GPU neighbours (two-grid x2 sweep): the sweep
-        // writes the outgoing PDFs of face / edge cells straight into the neighbour
-        // patches' ghost layers, replacing the ghost copies after the sweep.  Default
-        // on; LBM_LOCAL_DIRECT=0 keeps the copies.
+        // Direct ghost stores by the two-grid x2 sweep: face / edge cells write
+        // their outgoing PDFs straight into the neighbour patches' ghost layers.
+        // (1) same-GPU neighbours, replacing the ghost copies after the sweep
+        //     (default; LBM_LOCAL_DIRECT=0 keeps the copies);
+        // (2) with the fused exchange, the shells facing other GPUs are swept by
+        //     the same kernel through the peer-mapped table instead of the
+        //     one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell keeps it).
         const char *ev = std::getenv("LBM_LOCAL_DIRECT");
+        const char *es = std::getenv("LBM_SHELL_KERNEL");
         const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
-        const bool want = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && !ctx->lpull &&
-                          cfg->exchange_mode == LBM_EXCHANGE_AUTO && v >= 12 && !(ev && std::string(ev) == "0") &&
-                          !ctx->ex[EX_AB].segs.local.empty();
-        if (want) {
+        const bool x2 = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
+                        v >= 12;
+        const bool want_local = x2 && !ctx->lpull && !(ev && std::string(ev) == "0") &&
+                                !ctx->ex[EX_AB].segs.local.empty();
+        const bool want_shell = x2 && ctx->direct && !(es && std::string(es) == "onecell");
+        if (want_local || want_shell) {
             std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);
-            for (int l = 0; l < dec.nlocal; ++l) {
+            for (int l = 0; l < dec.nlocal && want_local; ++l) {
                 const int gp = dec.local_to_global(l);
                 for (int k = 0; k < NDIR; ++k) {
                     const int nbp = neighbour(dec, gp, kDirs[k].d);
@@ -1325,7 +1344,8 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             if (cudaMemcpy(ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
                 cudaSuccess)
                 return bail(LBM_ERR_CUDA);
-            ctx->ldirect = true;
+            ctx->ldirect = want_local;
+            ctx->x2_shells = want_shell;
         }
     }
     // Default geometry: closed no-slip box at rest (f~ = 0).

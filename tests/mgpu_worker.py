@@ -34,13 +34,15 @@ def main():
     # plus process grids that split x (the driver's 8-GPU run is 2x2x2)
     grids = {2: [(0, 0, 0), (2, 1, 1)], 4: [(0, 0, 0), (2, 2, 1), (2, 1, 2)]}.get(world, [(0, 0, 0)])
     # "fused_copies": fused exchange with same-GPU ghost copies instead of the
-    # sweep's direct ghost stores (LBM_LOCAL_DIRECT=0)
+    # sweep's direct ghost stores (LBM_LOCAL_DIRECT=0); "fused_onecell": remote
+    # shells swept by the one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell)
     combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "fused_copies", grids[0]),
+              (4, 1, 0, "fused_onecell", grids[0]),
               (8, 1, 0, "nccl", grids[0]),
               (8, 0, 0, "nccl", grids[0]), (4, 1, 0, "nccl", grids[0]), (8, 1, 1, "nccl", grids[0]),
               (4, 0, 1, "nccl", grids[0])]
     for pg in grids[1:]:
-        combos += [(8, 1, 0, "fused", pg), (8, 1, 0, "nccl", pg), (8, 1, 1, "nccl", pg)]
+        combos += [(8, 1, 0, "fused", pg), (4, 1, 0, "fused", pg), (8, 1, 0, "nccl", pg), (8, 1, 1, "nccl", pg)]
     for prec, overlap, layout, exch, pgrid in combos:
         if exch == "nccl":
             os.environ["LBM_EXCHANGE"] = "nccl"
@@ -50,6 +52,10 @@ def main():
             os.environ["LBM_LOCAL_DIRECT"] = "0"
         else:
             os.environ.pop("LBM_LOCAL_DIRECT", None)
+        if exch == "fused_onecell":
+            os.environ["LBM_SHELL_KERNEL"] = "onecell"
+        else:
+            os.environ.pop("LBM_SHELL_KERNEL", None)
         if True:
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
