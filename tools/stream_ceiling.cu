@@ -73,6 +73,69 @@ __global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ sr
     }
 }
 
+// fp32, four cells per thread: float4 for the 9 directions with e_x = 0, four
+// scalar loads for the pull-shifted ones; float4 stores.  Block (16, 8) = 64 x 8.
+template <bool SHIFT>
+__global__ void __launch_bounds__(128, 4) stream4_kernel(const float *__restrict__ src, float *__restrict__ dst, int n,
+                                                         int px, long long plane, long long qs, int xo)
+{
+    const int x0 = blockIdx.x * 64 + 4 * threadIdx.x;
+    const int y = blockIdx.y * 8 + threadIdx.y;
+    const int z = blockIdx.z % n;
+    const long long pbase = (long long)(blockIdx.z / n) * Q * qs;
+    if (x0 >= n || y >= n) return;
+    const long long cell = pbase + ((long long)(z + 1) * (n + 2) + (y + 1)) * px + x0 + xo;
+    float4 v[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const long long sh = SHIFT ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
+        const float *s = src + cell + i * qs - sh;
+        if (!SHIFT || cEX[i] == 0) {
+            v[i] = __ldg(reinterpret_cast<const float4 *>(s));
+        } else {
+            v[i].x = __ldg(s); v[i].y = __ldg(s + 1); v[i].z = __ldg(s + 2); v[i].w = __ldg(s + 3);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) *reinterpret_cast<float4 *>(dst + cell + i * qs) = v[i];
+}
+
+void run4(int n, int P)
+{
+    const int ae = 32, xo = ae;
+    const int px = ((xo + n + 2 + ae - 1) / ae) * ae;
+    const long long plane = (long long)px * (n + 2), qs = plane * (n + 2);
+    const size_t bytes = (size_t)P * Q * qs * sizeof(float);
+    float *a, *b;
+    cudaMalloc(&a, bytes);
+    cudaMalloc(&b, bytes);
+    cudaMemset(a, 0, bytes);
+    cudaMemset(b, 0, bytes);
+    dim3 grid((n + 63) / 64, (n + 7) / 8, n * P), block(16, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double alg = 2.0 * Q * sizeof(float) * (double)n * n * n * P;
+    for (int shift = 0; shift < 2; ++shift) {
+        for (int w = 0; w < 5; ++w)
+            shift ? stream4_kernel<true><<<grid, block>>>(a, b, n, px, plane, qs, xo)
+                  : stream4_kernel<false><<<grid, block>>>(a, b, n, px, plane, qs, xo);
+        const int reps = 50;
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r)
+            shift ? stream4_kernel<true><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo)
+                  : stream4_kernel<false><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("elem=4 n=%d patches=%d four cells/thread %s: %.3f ms/launch, %.1f GB/s algorithmic\n", n, P,
+               shift ? "pull-shifted" : "aligned", ms / reps, alg / (ms / reps * 1e-3) / 1e9);
+    }
+    cudaFree(a);
+    cudaFree(b);
+}
+
 template <typename T>
 __global__ void copy1d(const T *__restrict__ s, T *__restrict__ d, long long n)
 {
@@ -139,5 +202,6 @@ int main(int argc, char **argv)
     const int P = argc > 2 ? atoi(argv[2]) : 1;
     run<double>(n, P);
     run<float>(n, P);
+    run4(n, P);
     return 0;
 }
