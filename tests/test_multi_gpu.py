@@ -39,3 +39,18 @@ def test_nccl_exchange_matches_single_gpu(n):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+@pytest.mark.parametrize("n,config", [(2, "weak"), (4, "weak"), (2, "strong")])
+def test_full_size_bitwise_vs_one_gpu(n, config):
+    """BASELINE weak-scaling config (384^3 fp64 per GPU) and strong-scaling config
+    (768^3 in 8 patches of 384^3) at full size, 10 steps: N-GPU samples across
+    every process cut equal the one-GPU run bitwise (tests/mgpu_fullsize_worker.py)."""
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mgpu_fullsize_worker.py"), config]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
