@@ -137,17 +137,18 @@ def oracle_sample(nx, ny, target_s, threads):
         t0 = time.perf_counter()
         oracle.run(f0, fl, wu, inputs.LDC_OMEGA, steps, nthreads=threads)
         dt = time.perf_counter() - t0
-        if dt >= target_s or z >= 256:
+        if dt >= 0.7 * target_s or (z >= 256 and steps >= 64):
             cells = nx * ny * z
             return {"value": cells * steps / dt / 1e6, "unit": "MFLUPS", "cores": threads, "kind": "oracle",
                     "sample": f"oracle.run on a {nx}x{ny}x{z} LDC slab (lid on top), {steps} step(s), "
                               f"fp64, {threads} OpenMP threads, {dt:.2f} s"}
-        scale = max(2.0, min(16.0, target_s / max(dt, 1e-3)))
+        scale = max(1.2, min(16.0, 1.05 * target_s / max(dt, 1e-3)))
         if z * scale <= 256:
             z = int(z * scale)
-        else:
+        else:  # z capped: the steps take the rest of the factor
+            rest = z * scale / 256
             z = 256
-            steps = max(1, int(steps * scale))
+            steps = max(steps + 1, int(steps * rest))
 
 
 def run_reference(args):
@@ -326,7 +327,11 @@ def main():
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_{args.precision}.json")
     if os.path.exists(prof):
         with open(prof) as fh:
-            roofline["traffic"] = json.load(fh).get("dram_bytes_per_launch")
+            tr = json.load(fh)
+        roofline["traffic"] = tr.get("dram_bytes_per_launch")
+        if tr.get("gpu_time_us"):  # the ncu DRAM GB/s beside the algorithmic one
+            roofline["ncu_dram_gbs"] = tr["dram_bytes_per_launch"] / (tr["gpu_time_us"] * 1e-6) / 1e9
+    roofline["frac_spec"] = roofline["achieved"] / 8000.0  # against the 8 TB/s data-sheet figure
 
     # ---- end-to-end through the C ABI with host buffers
     e2e = None
@@ -405,11 +410,14 @@ def main():
                        "omega": inputs.LDC_OMEGA, "lid_u": inputs.LDC_U, "init": "dyadic noise seed 1388",
                        "overlap": bool(args.overlap), "graphs": bool(args.graphs), "layout": args.layout,
                        "exchange": "fused" if info["exchange_fused"] else "nccl",
+                       "same_gpu_exchange": ("direct ghost stores" if info["local_direct"] else
+                                             "local pull" if info["local_pull"] else
+                                             "ghost copies" if info["halo_bytes_local_per_step"] else "none"),
                        "l2": f"no flush: PDF state {2 * 19 * esize * fluid_local / 1e9:.2f} GB/GPU >> 126 MB L2",
                        "halo_bytes_remote_per_step": info["halo_bytes_remote_per_step"],
                        "row_pitch_elems": info["row_pitch_elems"], "align_bytes": info["align_bytes"]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks,
+            "clocks": clocks, "env": environment(),
             "model": {"source": "paper_1007_1388_b200/model.py (P:577-613 re-parameterised: HBM roofline + "
                                 "NVLink 770 GB/s halo)", **est},
         }
@@ -419,6 +427,34 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def environment() -> dict:
+    """GPU, driver, CUDA, NCCL and host CPU of this run (SURVEY 8(d) report record)."""
+    import platform
+    import torch
+    env = {"gpu": torch.cuda.get_device_name(), "cuda_runtime": torch.version.cuda, "torch": torch.__version__,
+           "host_cpu": platform.processor() or platform.machine(), "host_cores": len(os.sched_getaffinity(0))}
+    try:
+        env["nccl"] = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        env["nccl"] = None
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        env["driver"] = pynvml.nvmlSystemGetDriverVersion()
+        pynvml.nvmlShutdown()
+    except Exception:
+        env["driver"] = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    env["host_cpu"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return env
 
 
 if __name__ == "__main__":
