@@ -216,6 +216,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--proc-grid", default="", help="px,py,pz (default: split z, then y, then x)")
     args = ap.parse_args()
     if args.workload is None:
         args.workload = "ldc256"
@@ -245,6 +246,9 @@ def main():
     esize = 8 if prec == lbm.LBM_FP64 else 4
     brick, patch, kind = WORKLOADS[args.workload]
     pgrid = PROC_GRID.get(world, (1, 1, world))
+    if args.proc_grid:  # e.g. "2,1,1": exercise the x split of the 8-GPU grid on 2 GPUs
+        pgrid = tuple(int(v) for v in args.proc_grid.split(","))
+        assert len(pgrid) == 3 and pgrid[0] * pgrid[1] * pgrid[2] == world, "proc grid must multiply to N"
     if kind == "weak":
         domain = tuple(brick[a] * pgrid[a] for a in range(3))
     else:

@@ -137,7 +137,6 @@ struct lbm_ctx {
     bool has_nccl = false;     // a peer other than this rank
     ncclComm_t nccl = nullptr;
     DevBoxes box_all, box_shell, box_interior;
-    DevBoxes box_direct;   // fused exchange: remote-face shells first, then the rest
     bool use_overlap = false;
     int64_t fluid_local = 0, fluid_global = 0;
     bool flags_set = false;
@@ -272,6 +271,19 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
     CK(cudaMemcpy(out.boxes, boxes.data(), boxes.size() * sizeof(Box), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(out.prefix, prefix.data(), prefix.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     return LBM_OK;
+}
+
+void release_boxes(lbm_ctx *ctx, DevBoxes &b)
+{
+    if (b.boxes) {
+        cudaFree(b.boxes);
+        ctx->device_bytes -= (int64_t)(b.n * sizeof(Box));
+    }
+    if (b.prefix) {
+        cudaFree(b.prefix);
+        ctx->device_bytes -= (int64_t)((b.n + 1) * sizeof(int64_t));
+    }
+    b = DevBoxes{};
 }
 
 lbm_status upload_segs(lbm_ctx *ctx, const std::vector<CopySeg> &v, DevSegs &out)
@@ -450,28 +462,16 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
     return LBM_OK;
 }
 
-// Build the exchange plans, message buffers and sweep boxes.
-lbm_status setup_exchange(lbm_ctx *ctx)
+// Sweep boxes.  all: one box per local patch.  Overlap: for patches with
+// remote segments, a shell on every side a remote segment touches (1 cell
+// thick in y/z; SWEEP_BX thick in x so the shell rows stay coalesced) and the
+// remaining interior box.  whole_x (fused exchange): a patch with a remote x
+// side goes into the shell set whole -- an x slab splits every row between
+// two concurrently running kernels, which cost 9 % at 256^3 fp64 on a 2x1x1
+// process grid (row reads lose their DRAM page locality), while the fused
+// exchange has no transfer to hide behind the interior sweep.
+lbm_status build_boxes(lbm_ctx *ctx, bool whole_x)
 {
-    const bool aa = ctx->layout == LBM_LAYOUT_AA;
-    lbm_status st;
-    if ((st = setup_exset(ctx, EX_AB, !aa))) return st;
-    if ((st = setup_exset(ctx, EX_AA1, aa))) return st;
-    if ((st = setup_exset(ctx, EX_AA2, aa))) return st;
-    int64_t so = 0, ro = 0;
-    for (int k = 0; k < 3; ++k) {
-        so = std::max(so, ctx->ex[k].send_elems);
-        ro = std::max(ro, ctx->ex[k].recv_elems);
-    }
-    ctx->has_remote = ctx->ex[EX_AB].has_remote;
-    ctx->has_nccl = ctx->ex[EX_AB].has_nccl;
-    if ((st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize))) return st;
-    if ((st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize))) return st;
-
-    // Sweep boxes.  all: one box per local patch.  Overlap: for patches with
-    // remote segments, a shell on every side a remote segment touches (1 cell
-    // thick in y/z; SWEEP_BX thick in x so the shell rows stay coalesced) and
-    // the remaining interior box.
     std::vector<Box> all, shell, interior;
     const int *n = ctx->g.n;
     const int zero[3] = {0, 0, 0};
@@ -491,6 +491,10 @@ lbm_status setup_exchange(lbm_ctx *ctx)
         for (int k = 0; k < 6; ++k) any = any || side[6 * l + k];
         if (!any) {
             interior.push_back(make_box(ctx, l, zero, n));
+            continue;
+        }
+        if (whole_x && (side[6 * l] || side[6 * l + 1])) {
+            shell.push_back(make_box(ctx, l, zero, n));
             continue;
         }
         int th[6];
@@ -526,14 +530,33 @@ lbm_status setup_exchange(lbm_ctx *ctx)
             interior.push_back(make_box(ctx, l, lo, bn));
         }
     }
+    for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior}) release_boxes(ctx, *b);
+    lbm_status st;
     if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
     if ((st = upload_boxes(ctx, shell, ctx->box_shell))) return st;
     if ((st = upload_boxes(ctx, interior, ctx->box_interior))) return st;
-    {
-        std::vector<Box> direct(shell);
-        direct.insert(direct.end(), interior.begin(), interior.end());
-        if ((st = upload_boxes(ctx, direct, ctx->box_direct))) return st;
+    return LBM_OK;
+}
+
+// Build the exchange plans, message buffers and sweep boxes.
+lbm_status setup_exchange(lbm_ctx *ctx)
+{
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    lbm_status st;
+    if ((st = setup_exset(ctx, EX_AB, !aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA1, aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA2, aa))) return st;
+    int64_t so = 0, ro = 0;
+    for (int k = 0; k < 3; ++k) {
+        so = std::max(so, ctx->ex[k].send_elems);
+        ro = std::max(ro, ctx->ex[k].recv_elems);
     }
+    ctx->has_remote = ctx->ex[EX_AB].has_remote;
+    ctx->has_nccl = ctx->ex[EX_AB].has_nccl;
+    if ((st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize))) return st;
+    if ((st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize))) return st;
+
+    if ((st = build_boxes(ctx, false))) return st;
     ctx->use_overlap = ctx->cfg.overlap && ctx->has_nccl;
     return LBM_OK;
 }
@@ -978,8 +1001,7 @@ void destroy_ctx(lbm_ctx *ctx)
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
                     ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
-                    ctx->box_interior.boxes, ctx->box_interior.prefix, ctx->box_direct.boxes,
-                    ctx->box_direct.prefix};
+                    ctx->box_interior.boxes, ctx->box_interior.prefix};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->events_created)
@@ -1347,6 +1369,12 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             ctx->ldirect = want_local;
             ctx->x2_shells = want_shell;
         }
+    }
+    if (ctx->direct) {
+        // fused exchange: patches with a remote x side are swept whole (build_boxes);
+        // LBM_XSHELL=slab keeps the SWEEP_BX-wide x slabs
+        const char *ev = std::getenv("LBM_XSHELL");
+        if (!(ev && std::string(ev) == "slab") && (st = build_boxes(ctx, true))) return bail(st);
     }
     // Default geometry: closed no-slip box at rest (f~ = 0).
     {
