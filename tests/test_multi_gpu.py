@@ -29,16 +29,29 @@ def _port():
     return p
 
 
+_PORT_BUSY = ("Address already in use", "EADDRINUSE", "failed to listen", "address in use")
+
+
+def _torchrun(n, script, *args, timeout=600):
+    """torchrun on 127.0.0.1 with a free port; a port taken between the probe and
+    the rendezvous (another process, NCCL's bootstrap sockets) is retried."""
+    for attempt in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+               os.path.join(ROOT, "tests", script), *args]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+        busy = r.returncode != 0 and any(m in r.stdout + r.stderr for m in _PORT_BUSY)
+        if not busy:
+            break
+    print(r.stdout[-6000:], r.stderr[-6000:])
+    return r
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_nccl_exchange_matches_single_gpu(n):
     if _gpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mgpu_worker.py")]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0
+    assert _torchrun(n, "mgpu_worker.py").returncode == 0
 
 
 @pytest.mark.parametrize("n,config", [(2, "weak"), (4, "weak"), (2, "strong")])
@@ -48,9 +61,4 @@ def test_full_size_bitwise_vs_one_gpu(n, config):
     every process cut equal the one-GPU run bitwise (tests/mgpu_fullsize_worker.py)."""
     if _gpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mgpu_fullsize_worker.py"), config]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0
+    assert _torchrun(n, "mgpu_fullsize_worker.py", config, timeout=900).returncode == 0
