@@ -285,7 +285,9 @@ def test_local_pull_equals_ghost_copies(prec, monkeypatch):
 
 @pytest.mark.parametrize("prec", [8, 4])
 @pytest.mark.parametrize("n,patch,periodic", [((64, 30, 24), (16, 10, 12), (1, 0, 1)),
-                                              ((60, 30, 24), (15, 30, 8), (1, 1, 0))])
+                                              ((60, 30, 24), (15, 30, 8), (1, 1, 0)),
+                                              ((6, 4, 6), (1, 1, 2), (1, 1, 1)),
+                                              ((8, 6, 4), (2, 3, 1), (1, 0, 1))])
 def test_local_direct_equals_ghost_copies(prec, n, patch, periodic, monkeypatch):
     """The x2 sweep storing face / edge PDFs straight into same-GPU neighbour
     ghosts (the default) gives bitwise the ghost-copy result and the one-patch
