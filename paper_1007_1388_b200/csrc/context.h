@@ -1,0 +1,280 @@
+// context.h -- the per-rank runtime context and the helpers shared by the
+// runtime's translation units (private; the product interface is include/lbm.h):
+//   setup.cu     geometry, sweep boxes, exchange plans, flags, fused-exchange
+//                setup, create / destroy
+//   step.cu      one time step: sweep launches, ghost exchange, overlap,
+//                timing, CUDA graphs
+//   transfer.cu  host <-> device transfers of the canonical layout
+//   api.cu       the C ABI
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lbm_internal.h"
+
+namespace lbm {
+
+constexpr int kAlignDefault = 128;  // bytes; interior x = 0 of every row starts on this boundary
+constexpr int kTimingSlots = 64;
+enum Phase { PH_SWEEP = 0, PH_SHELL = 1, PH_INTERIOR = 2, PH_PACK = 3, PH_NCCL = 4, PH_UNPACK = 5, PH_STEP = 6 };
+constexpr int kEvPerSlot = 14;
+
+struct DevBoxes {
+    Box *boxes = nullptr;
+    int64_t *prefix = nullptr;
+    int n = 0;
+    int64_t tiles = 0;
+};
+
+struct DevSegs {
+    CopySeg *segs = nullptr;
+    int n = 0;
+    int64_t max_elems = 0;
+    int64_t total_elems = 0;
+};
+
+struct Peer {
+    int rank;
+    int64_t send_off, send_n, recv_off, recv_n;
+};
+
+// One exchange kind (EX_AB, EX_AA1, EX_AA2): segment lists, device copy
+// descriptors and the per-peer message layout.
+struct ExSet {
+    SegLists segs;
+    DevSegs pack_all;   // pack + local copies (non-overlapped step / ghost refresh)
+    DevSegs pack_remote, local_copy, unpack;
+    std::vector<CopySeg> h_pack_all, h_local, h_unpack;  // host copies (flag masks are refreshed)
+    std::vector<Peer> peers;
+    int64_t send_elems = 0, recv_elems = 0;
+    bool has_remote = false;   // anything goes through buffers
+    bool has_nccl = false;     // a peer other than this rank
+};
+
+struct TimingSlot {
+    cudaEvent_t ev[kEvPerSlot];
+    bool used = false;
+    bool overlap = false;
+    bool exchange = false;  // exchange phases were recorded (there was exchange work)
+};
+
+// file name without directories, for error messages
+inline const char *base_name(const char *path)
+{
+    const char *s = std::strrchr(path, '/');
+    return s ? s + 1 : path;
+}
+
+}  // namespace lbm
+
+using namespace lbm;
+
+struct lbm_ctx {
+    lbm_config cfg;
+    Decomp dec;
+    Geom g;
+    int esize = 8;
+    int device = 0;
+    int align = kAlignDefault;
+    // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
+    // two cells per thread with 2-vector accesses (x2): fp32 4 blocks/SM, fp64 3 blocks/SM (128 threads);
+    // env LBM_SWEEP_VARIANT.
+    int sweep_variant[2] = {12, 13};
+    int aa_variant[2] = {12, 13};  // AA kernels, two cells per thread (tools/sweep_tune.py --layout 1)
+    int direct_variant[2] = {6, 5};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
+    bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
+    int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
+    int num_sms = 148;
+    int tma_variant = 0;            // tile shape (sweep_tma.cu TmaShape); env LBM_TMA_SHAPE
+    alignas(64) CUtensorMap tm_pdf[2];
+    alignas(64) CUtensorMap tm_kind;
+    alignas(64) CUtensorMap tm_flags;
+    cudaStream_t stream = nullptr, comm_stream = nullptr;
+    // host <-> device transfers (transfer_chunks): two staging buffers and a
+    // copy stream, so the DMA of one chunk overlaps the kernel of the next
+    double *xstage[2] = {nullptr, nullptr};
+    size_t xstage_bytes = 0;
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t xev_copy[2] = {}, xev_kern[2] = {};
+    bool own_stream = false;
+    void *grid[2] = {nullptr, nullptr};
+    int cur = 0;
+    uint8_t *flags = nullptr, *kind = nullptr;
+    void *corr = nullptr;
+    int *d_origin = nullptr;
+    ExSet ex[3];               // indexed by ExKind
+    // Fused exchange (sweep_direct.cu): the sweep stores outgoing PDFs straight
+    // into neighbour ghost layers (local or CUDA-IPC-mapped peer memory).
+    bool direct = false;
+    void **d_nbr = nullptr;                 // [nlocal][18][2] neighbour patch bases
+    unsigned long long *d_epoch = nullptr;
+    unsigned long long *d_inbox = nullptr;  // [nranks] epochs published by the peers
+    unsigned long long **d_peer_inbox = nullptr;
+    int *d_peer_rank = nullptr;
+    int *d_error = nullptr;
+    int npeers_direct = 0;
+    std::vector<void *> ipc_mapped;         // peer grids / inboxes opened with cudaIpcOpenMemHandle
+    // Local pull (NEXT-2): face cells read same-GPU neighbour patches directly;
+    // no ghost copies between local patches.
+    bool lpull = false;
+    void **d_lnbr = nullptr;                // [nlocal][18][2]
+    // direct ghost stores by the x2 sweep (same-GPU and, with `direct`, peer patches)
+    bool ldirect = false;                   // same-GPU neighbours: no ghost copies
+    bool x2_shells = false;                 // fused exchange: shells swept by the x2 kernel
+    void **d_dnbr = nullptr;                // [nlocal][18][2]
+    std::vector<void *> h_nbr;              // setup_direct's peer-mapped table
+    int layout = LBM_LAYOUT_AB;
+    int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
+    void *sendbuf = nullptr, *recvbuf = nullptr;
+    bool has_remote = false;   // anything goes through buffers
+    bool has_nccl = false;     // a peer other than this rank
+    ncclComm_t nccl = nullptr;
+    DevBoxes box_all, box_shell, box_interior;
+    bool use_overlap = false;
+    int64_t fluid_local = 0, fluid_global = 0;
+    bool flags_set = false;
+    int64_t steps = 0, launches = 0;
+    int64_t launches_per_step = 0;
+    int64_t device_bytes = 0;
+    std::string err;
+    bool poisoned = false;
+    bool timing = false;
+    double phase_ms[LBM_NPHASES] = {0};
+    int64_t phase_count[LBM_NPHASES] = {0};
+    TimingSlot slots[kTimingSlots];
+    int slot_next = 0;
+    bool events_created = false;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    int64_t graph_launches[2] = {0, 0};
+
+    lbm_status fail(lbm_status st, const std::string &m)
+    {
+        err = m;
+        if (st == LBM_ERR_CUDA || st == LBM_ERR_NCCL || st == LBM_ERR_INTERNAL) poisoned = true;
+        return st;
+    }
+    lbm_status cuda_fail(cudaError_t e, const char *what, const char *file, int line)
+    {
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s [%s:%d]", cudaGetErrorName(e),
+                      cudaGetErrorString(e), what, base_name(file), line);
+        if (e == cudaErrorMemoryAllocation) {
+            err = buf;
+            return LBM_ERR_OOM;
+        }
+        return fail(LBM_ERR_CUDA, buf);
+    }
+    lbm_status nccl_fail(ncclResult_t r, const char *what, const char *file, int line)
+    {
+        char buf[512];
+        std::snprintf(buf, sizeof buf, "NCCL error %d (%s) in %s [%s:%d]", (int)r, ncclGetErrorString(r), what,
+                      base_name(file), line);
+        return fail(LBM_ERR_NCCL, buf);
+    }
+};
+
+#define CK(call)                                                              \
+    do {                                                                      \
+        cudaError_t e_ = (call);                                              \
+        if (e_ != cudaSuccess) return ctx->cuda_fail(e_, #call, __FILE__, __LINE__);    \
+    } while (0)
+#define NK(call)                                                              \
+    do {                                                                      \
+        ncclResult_t r_ = (call);                                             \
+        if (r_ != ncclSuccess) return ctx->nccl_fail(r_, #call, __FILE__, __LINE__);    \
+    } while (0)
+#define CHECK_CTX(ctx)                                                        \
+    do {                                                                      \
+        if (!(ctx)) return LBM_ERR_ARG;                                       \
+        if ((ctx)->poisoned) return LBM_ERR_STATE;                            \
+        cudaError_t e_ = cudaSetDevice((ctx)->device);                        \
+        if (e_ != cudaSuccess) return (ctx)->cuda_fail(e_, "cudaSetDevice", __FILE__, __LINE__); \
+    } while (0)
+
+namespace lbm {
+
+template <typename T>
+lbm_status dev_alloc(lbm_ctx *ctx, T **p, size_t bytes)
+{
+    *p = nullptr;
+    if (bytes == 0) return LBM_OK;
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+        ctx->err = buf;
+        return e == cudaErrorMemoryAllocation ? LBM_ERR_OOM : ctx->fail(LBM_ERR_CUDA, buf);
+    }
+    ctx->device_bytes += (int64_t)bytes;
+    return LBM_OK;
+}
+
+extern thread_local std::string g_create_error;  // api.cu: lbm_last_error(NULL)
+
+Geom make_geom(const int n[3], int esize, int align);
+
+Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3]);
+
+lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &out);
+
+void release_boxes(lbm_ctx *ctx, DevBoxes &b);
+
+lbm_status upload_segs(lbm_ctx *ctx, const std::vector<CopySeg> &v, DevSegs &out);
+
+CopySeg grid_to_x(const lbm_ctx *ctx, const Seg &s, bool to_buffer, int64_t buf_base);
+
+CopySeg buffer_to_grid(const lbm_ctx *ctx, const Seg &s, int64_t buf_base);
+
+lbm_status setup_exset(lbm_ctx *ctx, int kind, bool upload);
+
+lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags);
+
+lbm_status build_boxes(lbm_ctx *ctx, bool whole_x);
+
+lbm_status setup_exchange(lbm_ctx *ctx);
+
+lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u, int nvel);
+
+const char *validate_flags(const Decomp &dec, const uint8_t *flags, const double *wall_u, int nvel);
+
+void destroy_ctx(lbm_ctx *ctx);
+
+lbm_status setup_direct(lbm_ctx *ctx);
+
+lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out);
+
+lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s);
+
+lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *grid_dst, void *buf_src, void *buf_dst,
+                       cudaStream_t s);
+
+lbm_status transport(lbm_ctx *ctx, const ExSet &X, cudaStream_t s);
+
+lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, int kind, bool in_step);
+
+lbm_status refresh_state(lbm_ctx *ctx);
+
+lbm_status accumulate_slot(lbm_ctx *ctx, TimingSlot &ts);
+
+lbm_status flush_timing(lbm_ctx *ctx);
+
+lbm_status enqueue_step(lbm_ctx *ctx);
+
+lbm_status ensure_graph(lbm_ctx *ctx);
+
+lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n);
+
+lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode, double *rho, double *u);
+
+}  // namespace lbm

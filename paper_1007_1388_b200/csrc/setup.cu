@@ -1,0 +1,853 @@
+// setup.cu -- creating a rank's context: patch geometry (SoA with ghost shell,
+// P:1095-1124), the sweep box lists, the static ghost-exchange plans (P:287-313,
+// both sides derive identical offsets from lbm_plan), flags and the wall table
+// (P:482-490), the fused-exchange setup (CUDA IPC of the peers' grids) and the
+// direct ghost-store tables; destroy.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <new>
+
+#include "context.h"
+
+namespace lbm {
+
+Geom make_geom(const int n[3], int esize, int align)
+{
+    Geom g;
+    for (int a = 0; a < 3; ++a) g.n[a] = n[a];
+    const int ae = align / esize;             // elements per alignment unit
+    g.xo = ae;                                // x = -1 sits right before the aligned x = 0
+    // columns up to x = n + 1 must exist: the two-cells-per-thread kernels read
+    // the phantom partner x0 + 1 = n of an odd row and its pull neighbour n + 1
+    g.px = ((g.xo + n[0] + 2 + ae - 1) / ae) * ae;
+    g.py = n[1] + 2;
+    g.plane = (int64_t)g.px * g.py;
+    g.qs = g.plane * (n[2] + 2);
+    g.ps = (int64_t)Q * g.qs;
+    g.fs = g.qs;
+    return g;
+}
+
+Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3])
+{
+    Box b;
+    b.patch = patch;
+    for (int a = 0; a < 3; ++a) {
+        b.lo[a] = lo[a];
+        b.n[a] = n[a];
+    }
+    b.tiles_x = (n[0] + ctx->tile_x - 1) / ctx->tile_x;
+    b.tiles_y = (n[1] + ctx->tile_y - 1) / ctx->tile_y;
+    return b;
+}
+
+lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &out)
+{
+    std::vector<int64_t> prefix(boxes.size() + 1, 0);
+    for (size_t i = 0; i < boxes.size(); ++i) {
+        const Box &b = boxes[i];
+        const int zc = (ctx->use_tma || ctx->layout == LBM_LAYOUT_AA)
+                           ? 1
+                           : sweep_cells_z(ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]);
+        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0)
+                        ? (int64_t)b.tiles_x * b.tiles_y * ((b.n[2] + zc - 1) / zc)
+                        : 0;
+        prefix[i + 1] = prefix[i] + t;
+    }
+    out.n = (int)boxes.size();
+    out.tiles = prefix.back();
+    if (boxes.empty()) return LBM_OK;
+    lbm_status st = dev_alloc(ctx, &out.boxes, boxes.size() * sizeof(Box));
+    if (st) return st;
+    st = dev_alloc(ctx, &out.prefix, prefix.size() * sizeof(int64_t));
+    if (st) return st;
+    CK(cudaMemcpy(out.boxes, boxes.data(), boxes.size() * sizeof(Box), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(out.prefix, prefix.data(), prefix.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    return LBM_OK;
+}
+
+void release_boxes(lbm_ctx *ctx, DevBoxes &b)
+{
+    if (b.boxes) {
+        cudaFree(b.boxes);
+        ctx->device_bytes -= (int64_t)(b.n * sizeof(Box));
+    }
+    if (b.prefix) {
+        cudaFree(b.prefix);
+        ctx->device_bytes -= (int64_t)((b.n + 1) * sizeof(int64_t));
+    }
+    b = DevBoxes{};
+}
+
+lbm_status upload_segs(lbm_ctx *ctx, const std::vector<CopySeg> &v, DevSegs &out)
+{
+    out.n = (int)v.size();
+    out.max_elems = 0;
+    out.total_elems = 0;
+    for (const CopySeg &s : v) {
+        out.max_elems = std::max(out.max_elems, s.nelem);
+        out.total_elems += s.nelem;
+    }
+    if (v.empty()) return LBM_OK;
+    lbm_status st = dev_alloc(ctx, &out.segs, v.size() * sizeof(CopySeg));
+    if (st) return st;
+    CK(cudaMemcpy(out.segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+    return LBM_OK;
+}
+
+CopySeg grid_to_x(const lbm_ctx *ctx, const Seg &s, bool to_buffer, int64_t buf_base)
+{
+    // Source: the sender's boundary layer (a local patch); destination: either
+    // the receiver's ghost layer (local copy) or the send buffer.
+    CopySeg c;
+    std::memset(&c, 0, sizeof c);
+    const int lsend = ctx->dec.global_to_local(s.send_patch);
+    c.src_base = (int64_t)lsend * ctx->g.ps;
+    c.src_is_buf = 0;
+    for (int a = 0; a < 3; ++a) {
+        c.src_lo[a] = s.send_lo[a];
+        c.dst_lo[a] = s.recv_lo[a];
+        c.size[a] = s.size[a];
+    }
+    c.nq = s.nq;
+    for (int i = 0; i < 5; ++i) c.q[i] = i < s.nq ? s.q[i] : 0;
+    c.cells = s.cells;
+    c.nelem = (int64_t)s.nq * s.cells;
+    if (to_buffer) {
+        c.dst_is_buf = 1;
+        c.dst_base = buf_base + s.offset;
+    } else {
+        const int lrecv = ctx->dec.global_to_local(s.recv_patch);
+        c.dst_is_buf = 0;
+        c.dst_base = (int64_t)lrecv * ctx->g.ps;
+        c.dst_flag_base = (int64_t)lrecv * ctx->g.fs;
+    }
+    return c;
+}
+
+CopySeg buffer_to_grid(const lbm_ctx *ctx, const Seg &s, int64_t buf_base)
+{
+    CopySeg c;
+    std::memset(&c, 0, sizeof c);
+    const int lrecv = ctx->dec.global_to_local(s.recv_patch);
+    c.src_is_buf = 1;
+    c.src_base = buf_base + s.offset;
+    c.dst_is_buf = 0;
+    c.dst_base = (int64_t)lrecv * ctx->g.ps;
+    c.dst_flag_base = (int64_t)lrecv * ctx->g.fs;
+    for (int a = 0; a < 3; ++a) {
+        c.dst_lo[a] = s.recv_lo[a];
+        c.size[a] = s.size[a];
+    }
+    c.nq = s.nq;
+    for (int i = 0; i < 5; ++i) c.q[i] = i < s.nq ? s.q[i] : 0;
+    c.cells = s.cells;
+    c.nelem = (int64_t)s.nq * s.cells;
+    return c;
+}
+
+// Exchange plan of one kind: peers, message offsets, device copy descriptors.
+lbm_status setup_exset(lbm_ctx *ctx, int kind, bool upload)
+{
+    ExSet &X = ctx->ex[kind];
+    build_segments(ctx->dec, X.segs, kind);
+    std::vector<Peer> peers;
+    auto peer_of = [&](int r) -> Peer & {
+        for (Peer &p : peers)
+            if (p.rank == r) return p;
+        peers.push_back(Peer{r, 0, 0, 0, 0});
+        return peers.back();
+    };
+    for (const Seg &s : X.segs.send) peer_of(s.peer).send_n += (int64_t)s.nq * s.cells;
+    for (const Seg &s : X.segs.recv) peer_of(s.peer).recv_n += (int64_t)s.nq * s.cells;
+    std::sort(peers.begin(), peers.end(), [](const Peer &a, const Peer &b) { return a.rank < b.rank; });
+    int64_t so = 0, ro = 0;
+    for (Peer &p : peers) {
+        p.send_off = so;
+        p.recv_off = ro;
+        so += p.send_n;
+        ro += p.recv_n;
+    }
+    X.peers = peers;
+    X.send_elems = so;
+    X.recv_elems = ro;
+    X.has_remote = so > 0 || ro > 0;
+    X.has_nccl = false;
+    for (const Peer &p : peers)
+        if (p.rank != ctx->dec.rank) X.has_nccl = true;
+    if (!upload) return LBM_OK;
+
+    auto peer_send_off = [&](int r) {
+        for (const Peer &p : peers)
+            if (p.rank == r) return p.send_off;
+        return (int64_t)0;
+    };
+    auto peer_recv_off = [&](int r) {
+        for (const Peer &p : peers)
+            if (p.rank == r) return p.recv_off;
+        return (int64_t)0;
+    };
+    auto tag = [&](CopySeg c, const Seg &s) {
+        c.mask = kind == EX_AA2 ? 2 : 0;
+        for (int a = 0; a < 3; ++a) c.d[a] = s.d[a];
+        return c;
+    };
+    std::vector<CopySeg> pack_all, pack_remote, local, unpack;
+    for (const Seg &s : X.segs.send) {
+        CopySeg c = tag(grid_to_x(ctx, s, true, peer_send_off(s.peer)), s);
+        pack_all.push_back(c);
+        pack_remote.push_back(c);
+    }
+    for (const Seg &s : X.segs.local) {
+        CopySeg c = tag(grid_to_x(ctx, s, false, 0), s);
+        pack_all.push_back(c);
+        local.push_back(c);
+    }
+    for (const Seg &s : X.segs.recv) unpack.push_back(tag(buffer_to_grid(ctx, s, peer_recv_off(s.peer)), s));
+    lbm_status st;
+    if ((st = upload_segs(ctx, pack_all, X.pack_all))) return st;
+    if ((st = upload_segs(ctx, pack_remote, X.pack_remote))) return st;
+    if ((st = upload_segs(ctx, local, X.local_copy))) return st;
+    if ((st = upload_segs(ctx, unpack, X.unpack))) return st;
+    X.h_pack_all = pack_all;
+    X.h_local = local;
+    X.h_unpack = unpack;
+    return LBM_OK;
+}
+
+// After set_flags: a grid-destination segment whose destination cells are all
+// fluid needs no per-element flag check (mask 1).  The checks are half the DRAM
+// reads of the copy kernel on strided x faces (profiles/r01_ncu_copy_*).
+lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
+{
+    const Decomp &d = ctx->dec;
+    const int64_t NX = d.domain[0], NY = d.domain[1], NZ = d.domain[2];
+    auto all_fluid = [&](const CopySeg &c) {
+        const int l = (int)(c.dst_base / ctx->g.ps);
+        int pc[3];
+        d.patch_coord(d.local_to_global(l), pc);
+        for (int z = 0; z < c.size[2]; ++z)
+            for (int y = 0; y < c.size[1]; ++y)
+                for (int x = 0; x < c.size[0]; ++x) {
+                    int64_t gc[3] = {(int64_t)pc[0] * d.patch[0] + c.dst_lo[0] + x,
+                                     (int64_t)pc[1] * d.patch[1] + c.dst_lo[1] + y,
+                                     (int64_t)pc[2] * d.patch[2] + c.dst_lo[2] + z};
+                    const int64_t N[3] = {NX, NY, NZ};
+                    for (int a = 0; a < 3; ++a)
+                        if (d.periodic[a]) gc[a] = (gc[a] % N[a] + N[a]) % N[a];
+                    if (gflags[((gc[2] + 1) * (NY + 2) + (gc[1] + 1)) * (NX + 2) + (gc[0] + 1)] != 0) return false;
+                }
+        return true;
+    };
+    for (int k = 0; k < 3; ++k) {
+        ExSet &X = ctx->ex[k];
+        if (k == EX_AA2) continue;  // its mask also involves the writer cells
+        std::vector<CopySeg> *hv[3] = {&X.h_pack_all, &X.h_local, &X.h_unpack};
+        DevSegs *dv[3] = {&X.pack_all, &X.local_copy, &X.unpack};
+        for (int j = 0; j < 3; ++j) {
+            std::vector<CopySeg> &v = *hv[j];
+            if (v.empty() || !dv[j]->segs) continue;
+            for (CopySeg &c : v)
+                if (!c.dst_is_buf) c.mask = all_fluid(c) ? 1 : 0;
+            CK(cudaMemcpy(dv[j]->segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+        }
+    }
+    return LBM_OK;
+}
+
+// Sweep boxes.  all: one box per local patch.  Overlap: for patches with
+// remote segments, a shell on every side a remote segment touches (1 cell
+// thick in y/z; SWEEP_BX thick in x so the shell rows stay coalesced) and the
+// remaining interior box.  whole_x (fused exchange): a patch with a remote x
+// side goes into the shell set whole -- an x slab splits every row between
+// two concurrently running kernels, which cost 9 % at 256^3 fp64 on a 2x1x1
+// process grid (row reads lose their DRAM page locality), while the fused
+// exchange has no transfer to hide behind the interior sweep.
+lbm_status build_boxes(lbm_ctx *ctx, bool whole_x)
+{
+    std::vector<Box> all, shell, interior;
+    const int *n = ctx->g.n;
+    const int zero[3] = {0, 0, 0};
+    std::vector<int> side(6 * ctx->dec.nlocal, 0);
+    for (const Seg &s : ctx->ex[EX_AB].segs.send) {
+        const int l = ctx->dec.global_to_local(s.send_patch);
+        // s.d is the direction from the receiver to this (sending) patch; the
+        // sender's boundary layer is on side -s.d.
+        for (int a = 0; a < 3; ++a) {
+            if (s.d[a] == -1) side[6 * l + 2 * a + 1] = 1;  // high side of axis a
+            if (s.d[a] == 1) side[6 * l + 2 * a + 0] = 1;   // low side
+        }
+    }
+    for (int l = 0; l < ctx->dec.nlocal; ++l) {
+        all.push_back(make_box(ctx, l, zero, n));
+        bool any = false;
+        for (int k = 0; k < 6; ++k) any = any || side[6 * l + k];
+        if (!any) {
+            interior.push_back(make_box(ctx, l, zero, n));
+            continue;
+        }
+        if (whole_x && (side[6 * l] || side[6 * l + 1])) {
+            shell.push_back(make_box(ctx, l, zero, n));
+            continue;
+        }
+        int th[6];
+        for (int a = 0; a < 3; ++a) {
+            const int t = a == 0 ? ctx->tile_x : 1;
+            th[2 * a] = side[6 * l + 2 * a] ? std::min(t, n[a]) : 0;
+            th[2 * a + 1] = side[6 * l + 2 * a + 1] ? std::min(t, n[a] - th[2 * a]) : 0;
+        }
+        int lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = th[2 * a];
+            hi[a] = n[a] - th[2 * a + 1];
+        }
+        // Every tile must start on a 16-cell boundary in x (16-B aligned TMA
+        // starts for the PDF, kind and flag maps, see sweep_tma.cu): round the
+        // high-x shell start down.
+        const int xa = 16;
+        hi[0] = std::max(lo[0], hi[0] / xa * xa);
+        // z slabs (full xy), then y slabs (full x, inner z), then x slabs (inner y, z)
+        auto add = [&](int x0, int x1, int y0, int y1, int z0, int z1) {
+            if (x1 <= x0 || y1 <= y0 || z1 <= z0) return;
+            int blo[3] = {x0, y0, z0}, bn[3] = {x1 - x0, y1 - y0, z1 - z0};
+            shell.push_back(make_box(ctx, l, blo, bn));
+        };
+        add(0, n[0], 0, n[1], 0, lo[2]);
+        add(0, n[0], 0, n[1], hi[2], n[2]);
+        add(0, n[0], 0, lo[1], lo[2], hi[2]);
+        add(0, n[0], hi[1], n[1], lo[2], hi[2]);
+        add(0, lo[0], lo[1], hi[1], lo[2], hi[2]);
+        add(hi[0], n[0], lo[1], hi[1], lo[2], hi[2]);
+        if (hi[0] > lo[0] && hi[1] > lo[1] && hi[2] > lo[2]) {
+            int bn[3] = {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]};
+            interior.push_back(make_box(ctx, l, lo, bn));
+        }
+    }
+    for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior}) release_boxes(ctx, *b);
+    lbm_status st;
+    if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
+    if ((st = upload_boxes(ctx, shell, ctx->box_shell))) return st;
+    if ((st = upload_boxes(ctx, interior, ctx->box_interior))) return st;
+    return LBM_OK;
+}
+
+// Build the exchange plans, message buffers and sweep boxes.
+lbm_status setup_exchange(lbm_ctx *ctx)
+{
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    lbm_status st;
+    if ((st = setup_exset(ctx, EX_AB, !aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA1, aa))) return st;
+    if ((st = setup_exset(ctx, EX_AA2, aa))) return st;
+    int64_t so = 0, ro = 0;
+    for (int k = 0; k < 3; ++k) {
+        so = std::max(so, ctx->ex[k].send_elems);
+        ro = std::max(ro, ctx->ex[k].recv_elems);
+    }
+    ctx->has_remote = ctx->ex[EX_AB].has_remote;
+    ctx->has_nccl = ctx->ex[EX_AB].has_nccl;
+    if ((st = dev_alloc(ctx, &ctx->sendbuf, (size_t)so * ctx->esize))) return st;
+    if ((st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize))) return st;
+
+    if ((st = build_boxes(ctx, false))) return st;
+    ctx->use_overlap = ctx->cfg.overlap && ctx->has_nccl;
+    return LBM_OK;
+}
+
+lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u, int nvel)
+{
+    const int64_t nx = ctx->dec.domain[0], ny = ctx->dec.domain[1], nz = ctx->dec.domain[2];
+    const size_t total = (size_t)(nx + 2) * (ny + 2) * (nz + 2);
+    uint8_t *dflags = nullptr;
+    lbm_status st = dev_alloc(ctx, &dflags, total);
+    if (st) return st;
+    cudaError_t e = cudaMemcpy(dflags, flags, total, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = launch_build_flags(dflags, ctx->dec.domain, ctx->dec.periodic, ctx->d_origin, ctx->dec.nlocal, ctx->g,
+                               ctx->flags, ctx->kind, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(dflags);
+    ctx->device_bytes -= (int64_t)total;
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "build flags", __FILE__, __LINE__);
+    ctx->launches += 2 * ((ctx->dec.nlocal + 65534) / 65535);
+    // Wall correction table 6 w_i rho0 (e_i . u_w[k]) (R3, R9),
+    // computed in double and rounded once to the storage precision.
+    std::vector<double> cd((size_t)LBM_MAX_WALL_VELOCITIES * Q, 0.0);
+    for (int k = 0; k < nvel; ++k)
+        for (int i = 0; i < Q; ++i) {
+            const double eu = EX(i) * wall_u[3 * k] + EY(i) * wall_u[3 * k + 1] + EZ(i) * wall_u[3 * k + 2];
+            cd[(size_t)k * Q + i] = 6.0 * WQ(i) * 1.0 * eu;
+        }
+    if (ctx->esize == 8) {
+        CK(cudaMemcpy(ctx->corr, cd.data(), cd.size() * sizeof(double), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> cf(cd.begin(), cd.end());
+        CK(cudaMemcpy(ctx->corr, cf.data(), cf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    {
+        lbm_status st2 = update_seg_masks(ctx, flags);
+        if (st2) return st2;
+    }
+    // Fluid cell counts (MFLUPS counts fluid cells, R16).
+    int64_t gl = 0, lo = 0;
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y) {
+            const uint8_t *row = flags + ((z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + 1;
+            const bool zy_owned = z >= ctx->dec.owned_lo[2] && z < ctx->dec.owned_hi[2] && y >= ctx->dec.owned_lo[1] &&
+                                  y < ctx->dec.owned_hi[1];
+            for (int64_t x = 0; x < nx; ++x) {
+                if (row[x] == 0) {
+                    ++gl;
+                    if (zy_owned && x >= ctx->dec.owned_lo[0] && x < ctx->dec.owned_hi[0]) ++lo;
+                }
+            }
+        }
+    ctx->fluid_global = gl;
+    ctx->fluid_local = lo;
+    ctx->flags_set = true;
+    return LBM_OK;
+}
+
+const char *validate_flags(const Decomp &dec, const uint8_t *flags, const double *wall_u, int nvel)
+{
+    static thread_local char msg[256];
+    if (!flags) return "flags is NULL";
+    if (nvel < 0 || nvel > LBM_MAX_WALL_VELOCITIES) return "nvel must be in [0, 254]";
+    if (nvel > 0 && !wall_u) return "wall_u is NULL but nvel > 0";
+    for (int k = 0; k < 3 * nvel; ++k)
+        if (!std::isfinite(wall_u[k])) return "wall_u must be finite";
+    const int64_t nx = dec.domain[0], ny = dec.domain[1], nz = dec.domain[2];
+    for (int64_t z = -1; z <= nz; ++z)
+        for (int64_t y = -1; y <= ny; ++y) {
+            const uint8_t *row = flags + ((z + 1) * (ny + 2) + (y + 1)) * (nx + 2);
+            const bool yz_shell = (!dec.periodic[1] && (y < 0 || y >= ny)) || (!dec.periodic[2] && (z < 0 || z >= nz));
+            for (int64_t x = -1; x <= nx; ++x) {
+                const uint8_t f = row[x + 1];
+                const bool shell = yz_shell || (!dec.periodic[0] && (x < 0 || x >= nx));
+                if (shell && f == LBM_FLUID) {
+                    std::snprintf(msg, sizeof msg, "shell cell (%lld,%lld,%lld) on a non-periodic axis is fluid",
+                                  (long long)x, (long long)y, (long long)z);
+                    return msg;
+                }
+                if (f >= LBM_VELOCITY0 && f - LBM_VELOCITY0 >= nvel) {
+                    std::snprintf(msg, sizeof msg, "cell (%lld,%lld,%lld) has velocity wall %d but nvel = %d",
+                                  (long long)x, (long long)y, (long long)z, f - LBM_VELOCITY0, nvel);
+                    return msg;
+                }
+            }
+        }
+    return "";
+}
+
+void destroy_ctx(lbm_ctx *ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+    for (int i = 0; i < 2; ++i)
+        if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
+    if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
+    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_dnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
+                    (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
+        if (p) cudaFree(p);
+    for (ExSet &X : ctx->ex)
+        for (void *p : {(void *)X.pack_all.segs, (void *)X.pack_remote.segs, (void *)X.local_copy.segs,
+                        (void *)X.unpack.segs})
+            if (p) cudaFree(p);
+    void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
+                    ctx->recvbuf,
+                    ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
+                    ctx->box_interior.boxes, ctx->box_interior.prefix};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (ctx->events_created)
+        for (auto &sl : ctx->slots)
+            for (auto &ev : sl.ev) cudaEventDestroy(ev);
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->xstage[b]) cudaFree(ctx->xstage[b]);
+        if (ctx->xev_copy[b]) cudaEventDestroy(ctx->xev_copy[b]);
+        if (ctx->xev_kern[b]) cudaEventDestroy(ctx->xev_kern[b]);
+    }
+    if (ctx->xstream) cudaStreamDestroy(ctx->xstream);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    cudaGetLastError();
+    delete ctx;
+}
+
+// Fused-exchange setup: neighbour pointer table, epoch / inbox buffers and,
+// across GPUs, the CUDA IPC mapping of the peers' grids and inboxes (handles
+// all-gathered over the NCCL communicator).  All ranks agree on the outcome.
+lbm_status setup_direct(lbm_ctx *ctx)
+{
+    const Decomp &dec = ctx->dec;
+    const int R = dec.nranks, me = dec.rank;
+    lbm_status st;
+    if ((st = dev_alloc(ctx, &ctx->d_epoch, sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &ctx->d_inbox, (size_t)R * sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &ctx->d_error, sizeof(int)))) return st;
+    CK(cudaMemset(ctx->d_epoch, 0, sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
+    CK(cudaMemset(ctx->d_error, 0, sizeof(int)));
+    // Remote peers of the exchange plan.
+    std::vector<int> peers;
+    for (const Peer &p : ctx->ex[EX_AB].peers)
+        if (p.rank != me) peers.push_back(p.rank);
+    if (peers.empty()) return LBM_OK;  // nothing crosses a GPU boundary: copy path
+    std::vector<void *> peer_grid((size_t)R * 2, nullptr), peer_inbox((size_t)R, nullptr);
+    {
+        // all-gather {grid0, grid1, inbox} IPC handles
+        const size_t hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> mine(3);
+        CK(cudaIpcGetMemHandle(&mine[0], ctx->grid[0]));
+        CK(cudaIpcGetMemHandle(&mine[1], ctx->grid[1]));
+        CK(cudaIpcGetMemHandle(&mine[2], ctx->d_inbox));
+        char *dbuf = nullptr;
+        if ((st = dev_alloc(ctx, &dbuf, 3 * hb * (size_t)(R + 1)))) return st;
+        CK(cudaMemcpy(dbuf, mine.data(), 3 * hb, cudaMemcpyHostToDevice));
+        NK(ncclAllGather(dbuf, dbuf + 3 * hb, 3 * hb, ncclUint8, ctx->nccl, ctx->stream));
+        std::vector<cudaIpcMemHandle_t> all((size_t)3 * R);
+        CK(cudaMemcpyAsync(all.data(), dbuf + 3 * hb, 3 * hb * R, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dbuf);
+        ctx->device_bytes -= (int64_t)(3 * hb * (size_t)(R + 1));
+        int ok = 1;
+        for (int r : peers) {
+            for (int i = 0; i < 3 && ok; ++i) {
+                void *ptr = nullptr;
+                if (cudaIpcOpenMemHandle(&ptr, all[(size_t)3 * r + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    ok = 0;
+                    break;
+                }
+                ctx->ipc_mapped.push_back(ptr);
+                if (i < 2)
+                    peer_grid[(size_t)2 * r + i] = ptr;
+                else
+                    peer_inbox[r] = ptr;
+            }
+        }
+        // every rank must take the same path
+        int *dok = nullptr;
+        if ((st = dev_alloc(ctx, &dok, sizeof(int)))) return st;
+        CK(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+        NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->nccl, ctx->stream));
+        CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dok);
+        ctx->device_bytes -= (int64_t)sizeof(int);
+        if (!ok) return LBM_OK;  // stay on the NCCL exchange
+    }
+    // neighbour table
+    const int nl = dec.nlocal;
+    std::vector<void *> nbr((size_t)nl * NDIR * 2, nullptr);
+    for (int l = 0; l < nl; ++l) {
+        const int gpatch = dec.local_to_global(l);
+        for (int k = 0; k < NDIR; ++k) {
+            const int nbp = neighbour(dec, gpatch, kDirs[k].d);
+            if (nbp < 0) continue;
+            const int r = dec.owner(nbp);
+            if (r == me) continue;  // same-GPU neighbours: ghost copy after the sweep
+            const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+            for (int i = 0; i < 2; ++i) {
+                char *base = (char *)peer_grid[(size_t)2 * r + i];
+                nbr[((size_t)l * NDIR + k) * 2 + i] = base + off;
+            }
+        }
+    }
+    ctx->h_nbr = nbr;
+    if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
+    CK(cudaMemcpy(ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    std::vector<unsigned long long *> pin;
+    std::vector<int> prank;
+    for (int r : peers) {
+        pin.push_back((unsigned long long *)peer_inbox[r] + me);
+        prank.push_back(r);
+    }
+    ctx->npeers_direct = (int)peers.size();
+    if (!peers.empty()) {
+        if ((st = dev_alloc(ctx, &ctx->d_peer_inbox, pin.size() * sizeof(void *)))) return st;
+        CK(cudaMemcpy(ctx->d_peer_inbox, pin.data(), pin.size() * sizeof(void *), cudaMemcpyHostToDevice));
+        if ((st = dev_alloc(ctx, &ctx->d_peer_rank, prank.size() * sizeof(int)))) return st;
+        CK(cudaMemcpy(ctx->d_peer_rank, prank.data(), prank.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    ctx->direct = true;
+    return LBM_OK;
+}
+
+lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
+{
+    if (!out) return LBM_ERR_ARG;
+    *out = nullptr;
+    if (!cfg) {
+        g_create_error = "cfg is NULL";
+        return LBM_ERR_ARG;
+    }
+    Decomp dec;
+    const char *m = decompose(*cfg, dec);
+    if (m[0]) {
+        g_create_error = m;
+        return LBM_ERR_ARG;
+    }
+    if (cfg->nranks > 1 && !cfg->nccl_unique_id) {
+        g_create_error = "nccl_unique_id is required when nranks > 1";
+        return LBM_ERR_ARG;
+    }
+    lbm_ctx *ctx = new (std::nothrow) lbm_ctx();
+    if (!ctx) {
+        g_create_error = "host allocation failed";
+        return LBM_ERR_OOM;
+    }
+    ctx->cfg = *cfg;
+    ctx->dec = dec;
+    ctx->esize = cfg->precision;
+    ctx->layout = cfg->layout;
+    if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {
+        int v = std::atoi(a);
+        if (v >= 0 && v < kSweepVariants) {
+            ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
+        }
+        if ((v >= 0 && v < 8) || v >= 12) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
+        if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
+    }
+    if (const char *a = std::getenv("LBM_AA_VARIANT")) {  // AA kernels alone (12..15, kernels.cu launch_aa_x2)
+        int v = std::atoi(a);
+        if ((v >= 0 && v < 8) || (v >= 12 && v < kSweepVariants)) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
+    }
+    if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
+        if (std::string(a) == "simt") ctx->use_tma = false;
+        if (std::string(a) == "tma") ctx->use_tma = true;
+    }
+    if (ctx->layout == LBM_LAYOUT_AA) ctx->use_tma = false;  // the AA kernels are SIMT
+    if (const char *a = std::getenv("LBM_TMA_SHAPE")) {
+        int v = std::atoi(a);
+        if (v >= 0 && v <= 2) ctx->tma_variant = v;
+    }
+    if (ctx->use_tma) {
+        if (ctx->esize == 8)
+            tma_tile_shape<double>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
+        else
+            tma_tile_shape<float>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
+    }
+    if (const char *a = std::getenv("LBM_ALIGN_BYTES")) {
+        int v = std::atoi(a);
+        if (v >= ctx->esize && v <= 1024 && (v & (v - 1)) == 0) ctx->align = v;
+    }
+    auto bail = [&](lbm_status st) {
+        g_create_error = ctx->err.empty() ? "create failed" : ctx->err;
+        destroy_ctx(ctx);
+        return st;
+    };
+    // Device
+    int dev = cfg->device;
+    if (dev < 0) {
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+            return bail(LBM_ERR_CUDA);
+        }
+    }
+    ctx->device = dev;
+    {
+        cudaError_t e = cudaSetDevice(dev);
+        cudaDeviceProp prop;
+        if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+        if (e != cudaSuccess) {
+            ctx->err = std::string("cannot use CUDA device: ") + cudaGetErrorString(e);
+            cudaGetLastError();
+            return bail(LBM_ERR_CUDA);
+        }
+        if (prop.major != 10 || prop.minor != 0) {
+            ctx->err = "liblbm_b200 is built for sm_100a (B200); device " + std::to_string(dev) + " is " +
+                       std::string(prop.name) + " (sm_" + std::to_string(prop.major) + std::to_string(prop.minor) + ")";
+            return bail(LBM_ERR_CUDA);
+        }
+    }
+    ctx->g = make_geom(dec.patch, ctx->esize, ctx->align);
+    lbm_status st;
+    // Streams and events
+    if (cfg->stream) {
+        ctx->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate failed";
+            return bail(LBM_ERR_CUDA);
+        }
+        ctx->own_stream = true;
+    }
+    {
+        // The exchange stream gets the highest priority so the NCCL / unpack
+        // blocks are scheduled ahead of the interior sweep they overlap with.
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        if (cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
+            ctx->err = "cudaStreamCreate failed";
+            return bail(LBM_ERR_CUDA);
+        }
+    }
+    for (auto &sl : ctx->slots)
+        for (auto &ev : sl.ev)
+            if (cudaEventCreate(&ev) != cudaSuccess) {
+                ctx->err = "cudaEventCreate failed";
+                return bail(LBM_ERR_CUDA);
+            }
+    ctx->events_created = true;
+    // Memory budget check (clean OOM before the big allocations).
+    const size_t grid_bytes = (size_t)dec.nlocal * ctx->g.ps * ctx->esize;
+    const size_t flag_bytes = (size_t)dec.nlocal * ctx->g.fs;
+    const int ngrids = ctx->layout == LBM_LAYOUT_AA ? 1 : 2;
+    {
+        size_t freeb = 0, totalb = 0;
+        if (cudaMemGetInfo(&freeb, &totalb) == cudaSuccess && ngrids * grid_bytes + 2 * flag_bytes > freeb) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "need %.2f GB of device memory for the PDF grid(s) and flags, %.2f GB free",
+                          ((double)ngrids * grid_bytes + 2.0 * flag_bytes) / 1e9, freeb / 1e9);
+            ctx->err = buf;
+            return bail(LBM_ERR_OOM);
+        }
+    }
+    for (int i = 0; i < ngrids; ++i) {
+        if ((st = dev_alloc(ctx, &ctx->grid[i], grid_bytes))) return bail(st);
+        if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
+    }
+    if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->corr, (size_t)LBM_MAX_WALL_VELOCITIES * Q * ctx->esize))) return bail(st);
+    {
+        std::vector<int> origin(3 * dec.nlocal);
+        for (int l = 0; l < dec.nlocal; ++l) {
+            int c[3];
+            dec.patch_coord(dec.local_to_global(l), c);
+            for (int a = 0; a < 3; ++a) origin[3 * l + a] = c[a] * dec.patch[a];
+        }
+        if ((st = dev_alloc(ctx, &ctx->d_origin, origin.size() * sizeof(int)))) return bail(st);
+        if (cudaMemcpy(ctx->d_origin, origin.data(), origin.size() * sizeof(int), cudaMemcpyHostToDevice) !=
+            cudaSuccess)
+            return bail(LBM_ERR_CUDA);
+    }
+    {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            ctx->num_sms = sms;
+    }
+    if (ctx->use_tma) {
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t e = ctx->esize == 8
+                                ? make_tma_maps<double>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
+                                                        ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags)
+                                : make_tma_maps<float>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
+                                                       ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags);
+            if (e != cudaSuccess) {
+                ctx->err = "cuTensorMapEncodeTiled failed for the PDF / kind arrays";
+                return bail(LBM_ERR_CUDA);
+            }
+        }
+    }
+    if ((st = setup_exchange(ctx))) return bail(st);
+    // NCCL communicator (bootstrap id broadcast by the caller, e.g. torch.distributed)
+    if (cfg->nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->nccl, cfg->nranks, id, cfg->rank);
+        if (r != ncclSuccess) {
+            ctx->nccl = nullptr;
+            ctx->err = std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r);
+            return bail(LBM_ERR_NCCL);
+        }
+    }
+    {
+        // Fused exchange for the two-grid layout unless the NCCL path is requested
+        // (exchange_mode FORCE_BUFFERS, or env LBM_EXCHANGE=nccl).
+        const char *ev = std::getenv("LBM_EXCHANGE");
+        const bool want = ctx->layout == LBM_LAYOUT_AB && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
+                          !(ev && std::string(ev) == "nccl");
+        if (want && (st = setup_direct(ctx))) return bail(st);
+    }
+    {
+        // Local pull for the SIMT two-grid sweep when same-GPU neighbours exist.
+        // Opt-in: measured slower than the ghost copies on B200.
+        const char *ev = std::getenv("LBM_LOCAL_PULL");
+        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
+        const bool want = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && !ctx->direct &&
+                          cfg->exchange_mode == LBM_EXCHANGE_AUTO && v >= 4 && v < 8 &&
+                          (ev && std::string(ev) == "1") && !ctx->ex[EX_AB].segs.local.empty();
+        if (want) {
+            std::vector<void *> tab((size_t)dec.nlocal * NDIR * 2, nullptr);
+            for (int l = 0; l < dec.nlocal; ++l) {
+                const int gp = dec.local_to_global(l);
+                for (int k = 0; k < NDIR; ++k) {
+                    const int nbp = neighbour(dec, gp, kDirs[k].d);
+                    if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
+                    const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
+                }
+            }
+            if ((st = dev_alloc(ctx, &ctx->d_lnbr, tab.size() * sizeof(void *)))) return bail(st);
+            if (cudaMemcpy(ctx->d_lnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+                return bail(LBM_ERR_CUDA);
+            ctx->lpull = true;
+        }
+    }
+    {
+        // Direct ghost stores by the two-grid x2 sweep: face / edge cells write
+        // their outgoing PDFs straight into the neighbour patches' ghost layers.
+        // (1) same-GPU neighbours, replacing the ghost copies after the sweep
+        //     (default; LBM_LOCAL_DIRECT=0 keeps the copies);
+        // (2) with the fused exchange, the shells facing other GPUs are swept by
+        //     the same kernel through the peer-mapped table instead of the
+        //     one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell keeps it).
+        const char *ev = std::getenv("LBM_LOCAL_DIRECT");
+        const char *es = std::getenv("LBM_SHELL_KERNEL");
+        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
+        const bool x2 = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
+                        v >= 12;
+        const bool want_local = x2 && !ctx->lpull && !(ev && std::string(ev) == "0") &&
+                                !ctx->ex[EX_AB].segs.local.empty();
+        const bool want_shell = x2 && ctx->direct && !(es && std::string(es) == "onecell");
+        if (want_local || want_shell) {
+            std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);
+            for (int l = 0; l < dec.nlocal && want_local; ++l) {
+                const int gp = dec.local_to_global(l);
+                for (int k = 0; k < NDIR; ++k) {
+                    const int nbp = neighbour(dec, gp, kDirs[k].d);
+                    if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
+                    const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
+                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
+                }
+            }
+            if ((st = dev_alloc(ctx, &ctx->d_dnbr, tab.size() * sizeof(void *)))) return bail(st);
+            if (cudaMemcpy(ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+                cudaSuccess)
+                return bail(LBM_ERR_CUDA);
+            ctx->ldirect = want_local;
+            ctx->x2_shells = want_shell;
+        }
+    }
+    if (ctx->direct) {
+        // fused exchange: patches with a remote x side are swept whole (build_boxes);
+        // LBM_XSHELL=slab keeps the SWEEP_BX-wide x slabs
+        const char *ev = std::getenv("LBM_XSHELL");
+        if (!(ev && std::string(ev) == "slab") && (st = build_boxes(ctx, true))) return bail(st);
+    }
+    // Default geometry: closed no-slip box at rest (f~ = 0).
+    {
+        const int64_t nx = dec.domain[0], ny = dec.domain[1], nz = dec.domain[2];
+        std::vector<uint8_t> fl((size_t)(nx + 2) * (ny + 2) * (nz + 2), 0);
+        for (int64_t z = -1; z <= nz; ++z)
+            for (int64_t y = -1; y <= ny; ++y)
+                for (int64_t x = -1; x <= nx; ++x) {
+                    const bool shell = x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz;
+                    if (shell) fl[((z + 1) * (ny + 2) + (y + 1)) * (nx + 2) + (x + 1)] = LBM_NOSLIP;
+                }
+        if ((st = apply_flags(ctx, fl.data(), nullptr, 0))) return bail(st);
+    }
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
+    *out = ctx;
+    return LBM_OK;
+}
+
+}  // namespace lbm

@@ -1,0 +1,351 @@
+// step.cu -- one time step (the paper's Sweep) on a rank: sweep
+// (fused pull + BB + collide, kernels.cu) and ghost exchange -- folded into the
+// sweep as direct ghost stores (same GPU and, fused, NVLink stores into the
+// peers' grids with one epoch handshake), or extract -> NCCL -> insert
+// (P:287-313), shells first and overlapped with the interiors (the
+// paper sums these times).  Step pairs are captured in CUDA graphs.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <new>
+
+#include "context.h"
+
+namespace lbm {
+
+template <typename real>
+SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
+{
+    SweepArgs<real> a;
+    if (ctx->layout == LBM_LAYOUT_AA) {  // in place
+        a.src = (const real *)ctx->grid[0];
+        a.dst = (real *)ctx->grid[0];
+    } else {
+        a.src = (const real *)ctx->grid[ctx->cur];
+        a.dst = (real *)ctx->grid[1 - ctx->cur];
+    }
+    a.flags = ctx->flags;
+    a.kind = ctx->kind;
+    a.corr = (const real *)ctx->corr;
+    a.g = ctx->g;
+    a.omega = (real)ctx->cfg.omega;
+    a.boxes = b.boxes;
+    a.tile_prefix = b.prefix;
+    a.nboxes = b.n;
+    a.lnbr = ctx->lpull ? (const real *const *)ctx->d_lnbr : nullptr;
+    a.srci = ctx->cur;
+    a.dnbr = ctx->ldirect && ctx->layout == LBM_LAYOUT_AB ? (real *const *)ctx->d_dnbr : nullptr;
+    a.dsti = 1 - ctx->cur;
+    return a;
+}
+
+lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
+{
+    if (b.tiles == 0) return LBM_OK;
+    cudaError_t e;
+    if (ctx->layout == LBM_LAYOUT_AA) {
+        const bool pull = ctx->aa_phase == 0;
+        if (ctx->esize == 8)
+            e = launch_sweep_aa<double>(sweep_args<double>(ctx, b), b.tiles, pull, ctx->aa_variant[1], s);
+        else
+            e = launch_sweep_aa<float>(sweep_args<float>(ctx, b), b.tiles, pull, ctx->aa_variant[0], s);
+    } else if (ctx->use_tma) {
+        const CUtensorMap &pm = ctx->tm_pdf[ctx->cur];
+        if (ctx->esize == 8)
+            e = launch_sweep_tma<double>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
+                                         ctx->num_sms, ctx->tma_variant, s);
+        else
+            e = launch_sweep_tma<float>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<float>(ctx, b), b.tiles,
+                                        ctx->num_sms, ctx->tma_variant, s);
+    } else if (ctx->esize == 8)
+        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant[1], s);
+    else
+        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, ctx->sweep_variant[0], s);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_kernel launch", __FILE__, __LINE__);
+    ctx->launches += 1;
+    return LBM_OK;
+}
+
+lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *grid_dst, void *buf_src, void *buf_dst,
+                       cudaStream_t s)
+{
+    if (d.n == 0 || d.max_elems == 0) return LBM_OK;
+    cudaError_t e;
+    if (ctx->esize == 8)
+        e = launch_copy_segments<double>(d.segs, d.n, d.max_elems, (const double *)grid_src, (double *)grid_dst,
+                                         (const double *)buf_src, (double *)buf_dst, ctx->flags, ctx->g, s);
+    else
+        e = launch_copy_segments<float>(d.segs, d.n, d.max_elems, (const float *)grid_src, (float *)grid_dst,
+                                        (const float *)buf_src, (float *)buf_dst, ctx->flags, ctx->g, s);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "copy_segments launch", __FILE__, __LINE__);
+    ctx->launches += (d.n + 65534) / 65535;
+    return LBM_OK;
+}
+
+// Transport of the send buffers: grouped NCCL send/recv per peer;
+// a self-peer (exchange_mode FORCE_BUFFERS) is a device copy.
+lbm_status transport(lbm_ctx *ctx, const ExSet &X, cudaStream_t s)
+{
+    const ncclDataType_t dt = ctx->esize == 8 ? ncclFloat64 : ncclFloat32;
+    char *sb = (char *)ctx->sendbuf, *rb = (char *)ctx->recvbuf;
+    for (const Peer &p : X.peers)
+        if (p.rank == ctx->dec.rank && p.send_n > 0)
+            CK(cudaMemcpyAsync(rb + p.recv_off * ctx->esize, sb + p.send_off * ctx->esize, p.send_n * ctx->esize,
+                               cudaMemcpyDeviceToDevice, s));
+    if (!X.has_nccl) return LBM_OK;
+    NK(ncclGroupStart());
+    for (const Peer &p : X.peers) {
+        if (p.rank == ctx->dec.rank) continue;
+        if (p.send_n > 0) NK(ncclSend(sb + p.send_off * ctx->esize, (size_t)p.send_n, dt, p.rank, ctx->nccl, s));
+        if (p.recv_n > 0) NK(ncclRecv(rb + p.recv_off * ctx->esize, (size_t)p.recv_n, dt, p.rank, ctx->nccl, s));
+    }
+    NK(ncclGroupEnd());
+    return LBM_OK;
+}
+
+// Ghost refresh of grid `gi` (used after set_pdfs / init and inside the step).
+// in_step: right after a sweep, whose direct stores (ldirect) already filled
+// the same-GPU ghosts.
+lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, int kind, bool in_step)
+{
+    void *grid = ctx->grid[gi];
+    const ExSet &X = ctx->ex[kind];
+    lbm_status st;
+    // local pull: same-GPU neighbours are read in place, only remote segments move
+    const bool skip_local = ctx->lpull || (in_step && ctx->ldirect);
+    const bool work = (skip_local ? X.pack_remote.n : X.pack_all.n) > 0 || X.has_remote || X.unpack.n > 0;
+    if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
+    if (ts) ts->exchange = true;
+    if (ts) CK(cudaEventRecord(ts->ev[2], s));
+    if ((st = launch_copy(ctx, skip_local ? X.pack_remote : X.pack_all, grid, grid, nullptr, ctx->sendbuf, s)))
+        return st;
+    if (ts) CK(cudaEventRecord(ts->ev[3], s));
+    if (X.has_remote) {
+        if ((st = transport(ctx, X, s))) return st;
+    }
+    if (ts) CK(cudaEventRecord(ts->ev[4], s));
+    if ((st = launch_copy(ctx, X.unpack, nullptr, grid, ctx->recvbuf, nullptr, s))) return st;
+    if (ts) CK(cudaEventRecord(ts->ev[5], s));
+    return LBM_OK;
+}
+
+// After the state or the flags change: refresh the ghost layers of the current
+// grid and park the store-side bounce-back values in the wall cells.
+lbm_status refresh_state(lbm_ctx *ctx)
+{
+    // AB: ghost layers of the current grid.  AA (swapped state): half-exchange 1,
+    // which is what the next PULL step gathers from the ghost layers.
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB, false);
+    if (st) return st;
+    cudaError_t e = ctx->esize == 8
+                        ? launch_bb_fill<double>((double *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
+                                                 (const double *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
+                                                 ctx->stream)
+                        : launch_bb_fill<float>((float *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
+                                                (const float *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
+                                                ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "bb_fill", __FILE__, __LINE__);
+    ctx->launches += (ctx->dec.nlocal + 65534) / 65535;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return LBM_OK;
+}
+
+lbm_status accumulate_slot(lbm_ctx *ctx, TimingSlot &ts)
+{
+    if (!ts.used) return LBM_OK;
+    CK(cudaEventSynchronize(ts.ev[kEvPerSlot - 1]));
+    auto el = [&](int a, int b) -> double {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ts.ev[a], ts.ev[b]);
+        return (double)ms;
+    };
+    if (!ts.overlap) {
+        ctx->phase_ms[PH_SWEEP] += el(0, ts.exchange ? 2 : kEvPerSlot - 1);
+        ctx->phase_count[PH_SWEEP] += 1;
+        if (ts.exchange) {
+            ctx->phase_ms[PH_PACK] += el(2, 3);
+            ctx->phase_ms[PH_NCCL] += el(3, 4);
+            ctx->phase_ms[PH_UNPACK] += el(4, 5);
+            ctx->phase_count[PH_PACK] += 1;
+            ctx->phase_count[PH_NCCL] += 1;
+            ctx->phase_count[PH_UNPACK] += 1;
+        }
+    } else {
+        ctx->phase_ms[PH_SHELL] += el(0, 2);
+        ctx->phase_ms[PH_PACK] += el(2, 3);
+        ctx->phase_ms[PH_NCCL] += el(6, 7);
+        ctx->phase_ms[PH_UNPACK] += el(7, 8);
+        ctx->phase_ms[PH_INTERIOR] += el(3, 9);
+        for (int p : {PH_SHELL, PH_PACK, PH_NCCL, PH_UNPACK, PH_INTERIOR}) ctx->phase_count[p] += 1;
+    }
+    ctx->phase_ms[PH_STEP] += el(0, kEvPerSlot - 1);
+    ctx->phase_count[PH_STEP] += 1;
+    ts.used = false;
+    cudaGetLastError();
+    return LBM_OK;
+}
+
+lbm_status flush_timing(lbm_ctx *ctx)
+{
+    for (int i = 0; i < kTimingSlots; ++i) {
+        lbm_status st = accumulate_slot(ctx, ctx->slots[i]);
+        if (st) return st;
+    }
+    return LBM_OK;
+}
+
+// Enqueue one time step grid[cur] -> grid[1-cur] and flip cur.
+lbm_status enqueue_step(lbm_ctx *ctx)
+{
+    cudaStream_t s = ctx->stream;
+    TimingSlot *ts = nullptr;
+    lbm_status st;
+    if (ctx->timing) {
+        ts = &ctx->slots[ctx->slot_next];
+        ctx->slot_next = (ctx->slot_next + 1) % kTimingSlots;
+        if ((st = accumulate_slot(ctx, *ts))) return st;
+        ts->used = true;
+        ts->overlap = ctx->use_overlap && !ctx->direct;
+        ts->exchange = false;
+        CK(cudaEventRecord(ts->ev[0], s));
+    }
+    // AB: grid[cur] -> grid[1-cur], exchange of the pulled PDFs.  AA: in place
+    // on grid[0]; a PULL step is followed by half-exchange 2, a LOCAL step by 1.
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    const int dsti = aa ? 0 : 1 - ctx->cur;
+    const int kind = aa ? (ctx->aa_phase == 0 ? EX_AA2 : EX_AA1) : EX_AB;
+    const ExSet &X = ctx->ex[kind];
+    void *dst = ctx->grid[dsti];
+    if (ctx->direct) {
+        // Fused exchange across GPUs.  C (high priority): wait for the peers' epoch,
+        // sweep the shells facing remote neighbours with the fused kernel (NVLink
+        // stores of the outgoing PDFs into the peers' ghost layers), publish the
+        // epoch.  S, concurrently: the plain sweep of everything else.  Then S joins
+        // C and copies the ghosts between same-GPU patches.
+        cudaStream_t c = ctx->comm_stream;
+        cudaEvent_t ev_start = ts ? ts->ev[10] : ctx->slots[0].ev[10];
+        cudaEvent_t ev_shell = ts ? ts->ev[11] : ctx->slots[0].ev[11];
+        CK(cudaEventRecord(ev_start, s));
+        CK(cudaStreamWaitEvent(c, ev_start, 0));
+        cudaError_t e = launch_wait_peers(ctx->d_inbox, ctx->d_peer_rank, ctx->npeers_direct, ctx->d_epoch,
+                                          ctx->d_error, c);
+        if (e != cudaSuccess) return ctx->cuda_fail(e, "wait_peers launch", __FILE__, __LINE__);
+        ctx->launches += 1;
+        const DevBoxes &bs = ctx->box_shell;
+        if (bs.tiles > 0 && ctx->x2_shells) {
+            if (ctx->esize == 8) {
+                SweepArgs<double> a = sweep_args<double>(ctx, bs);
+                a.dnbr = (double *const *)ctx->d_dnbr;
+                e = launch_sweep<double>(a, bs.tiles, ctx->sweep_variant[1], c);
+            } else {
+                SweepArgs<float> a = sweep_args<float>(ctx, bs);
+                a.dnbr = (float *const *)ctx->d_dnbr;
+                e = launch_sweep<float>(a, bs.tiles, ctx->sweep_variant[0], c);
+            }
+            if (e != cudaSuccess) return ctx->cuda_fail(e, "shell sweep launch", __FILE__, __LINE__);
+            ctx->launches += 1;
+        } else if (bs.tiles > 0) {
+            void **tab = ctx->ldirect ? ctx->d_dnbr : ctx->d_nbr;
+            if (ctx->esize == 8) {
+                DirectArgs<double> dx{(double *const *)tab, dsti};
+                e = launch_sweep_direct<double>(sweep_args<double>(ctx, bs), dx, bs.tiles, ctx->direct_variant[1], c);
+            } else {
+                DirectArgs<float> dx{(float *const *)tab, dsti};
+                e = launch_sweep_direct<float>(sweep_args<float>(ctx, bs), dx, bs.tiles, ctx->direct_variant[0], c);
+            }
+            if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_direct launch", __FILE__, __LINE__);
+            ctx->launches += 1;
+        }
+        e = launch_signal_peers(ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct, c);
+        if (e != cudaSuccess) return ctx->cuda_fail(e, "signal_peers launch", __FILE__, __LINE__);
+        ctx->launches += 1;
+        CK(cudaEventRecord(ev_shell, c));
+        if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
+        CK(cudaStreamWaitEvent(s, ev_shell, 0));
+        if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
+    } else if (!ctx->use_overlap) {
+        if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
+        if ((st = exchange_seq(ctx, dsti, s, ts, kind, true))) return st;
+    } else {
+        cudaStream_t c = ctx->comm_stream;
+        // S: shells facing remote neighbours, then pack them.
+        if ((st = launch_sweep_set(ctx, ctx->box_shell, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[2], s));
+        if ((st = launch_copy(ctx, X.pack_remote, dst, dst, nullptr, ctx->sendbuf, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[3], s));
+        CK(cudaEventRecord(ts ? ts->ev[10] : ctx->slots[0].ev[10], s));
+        // C: transport + unpack while S sweeps the interiors.
+        CK(cudaStreamWaitEvent(c, ts ? ts->ev[10] : ctx->slots[0].ev[10], 0));
+        if (ts) CK(cudaEventRecord(ts->ev[6], c));
+        if ((st = transport(ctx, X, c))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[7], c));
+        if ((st = launch_copy(ctx, X.unpack, nullptr, dst, ctx->recvbuf, nullptr, c))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[8], c));
+        CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
+        if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
+        if (ts) CK(cudaEventRecord(ts->ev[9], s));
+        if (!ctx->lpull && !ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
+            return st;
+        CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
+    }
+    if (ts) CK(cudaEventRecord(ts->ev[kEvPerSlot - 1], s));
+    if (aa)
+        ctx->aa_phase ^= 1;
+    else
+        ctx->cur = dsti;
+    ctx->steps += 1;
+    return LBM_OK;
+}
+
+lbm_status ensure_graph(lbm_ctx *ctx)
+{
+    // AB: one graph per starting grid; AA: one graph, starting from the swapped phase.
+    const int c = ctx->layout == LBM_LAYOUT_AA ? 0 : ctx->cur;
+    if (ctx->graph[c]) return LBM_OK;
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = ctx->launches, s0 = ctx->steps;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    lbm_status st = enqueue_step(ctx);
+    if (!st) st = enqueue_step(ctx);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    if (st) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+    ctx->graph_launches[c] = ctx->launches - l0;
+    ctx->launches = l0;
+    ctx->steps = s0;  // capture did not execute anything
+    // cur flipped twice -> back to c
+    e = cudaGraphInstantiate(&ctx->graph[c], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        ctx->graph[c] = nullptr;
+        return ctx->cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+    }
+    return LBM_OK;
+}
+
+lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n)
+{
+    lbm_status st;
+    const bool graphs = ctx->cfg.use_graphs && !ctx->timing;
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    while (n > 0) {
+        if (graphs && n >= 2 && !(aa && ctx->aa_phase != 0)) {
+            if ((st = ensure_graph(ctx))) return st;
+            const int gidx = aa ? 0 : ctx->cur;
+            CK(cudaGraphLaunch(ctx->graph[gidx], ctx->stream));
+            ctx->launches += ctx->graph_launches[gidx];
+            ctx->steps += 2;
+            n -= 2;
+        } else {
+            if ((st = enqueue_step(ctx))) return st;
+            n -= 1;
+        }
+    }
+    return LBM_OK;
+}
+
+}  // namespace lbm
