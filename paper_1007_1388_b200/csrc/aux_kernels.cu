@@ -1,0 +1,421 @@
+// aux_kernels.cu -- the non-sweep kernels: ghost-exchange copies (pack /
+// local copy / unpack), flags and cell kinds, canonical import /
+// export and macroscopic moments, the seeded noise initialiser, the
+// sampled gather and the store-side bounce-back fill.
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "sweep_common.cuh"
+
+namespace lbm {
+
+// ---------------------------------------------------------------- ghost exchange copies
+// Non-fluid destination cells are skipped: their PDF slots hold the store-side
+// bounce-back values written by the receiving patch itself.
+template <typename real>
+__global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs, const real *grid_src,
+                                                            real *grid_dst, const real *buf_src,
+                                                            real *buf_dst, const uint8_t *flags, const Geom g)
+{
+    const CopySeg &sg = segs[blockIdx.y];
+    // 32-bit element decomposition (a segment has < 2^31 elements).
+    const int nelem = (int)sg.nelem, cells = (int)sg.cells;
+    const int s0 = sg.size[0], s1 = sg.size[1];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nelem; e += gridDim.x * blockDim.x) {
+        const int qi = e / cells;
+        const int c = e - qi * cells;
+        const int r = c / s0;
+        const int cx = c - r * s0;
+        const int cz = r / s1;
+        const int cy = r - cz * s1;
+        const int q = sg.q[qi];
+        real v;
+        if (sg.src_is_buf)
+            v = buf_src[sg.src_base + e];
+        else
+            v = grid_src[sg.src_base + q * g.qs +
+                         cell_index(g, sg.src_lo[0] + cx, sg.src_lo[1] + cy, sg.src_lo[2] + cz)];
+        if (sg.dst_is_buf) {
+            buf_dst[sg.dst_base + e] = v;
+        } else {
+            const int y[3] = {sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz};
+            const int64_t ci = cell_index(g, y[0], y[1], y[2]);
+            bool ok = sg.mask == 1 || flags[sg.dst_flag_base + ci] == 0;  // mask 1: all destinations fluid
+            if (sg.mask == 2 && ok) {
+                // AA half-exchange 2: the value was scattered by the sender's cell
+                // w = y - e_q; only entries whose writer is a fluid cell of the
+                // sender (not another patch's ghost) are delivered.
+                const int w[3] = {y[0] - EX(q), y[1] - EY(q), y[2] - EZ(q)};
+                for (int a2 = 0; a2 < 3; ++a2)
+                    if (sg.d[a2] == 0 && (w[a2] < 0 || w[a2] >= g.n[a2])) ok = false;
+                if (ok) ok = flags[sg.dst_flag_base + cell_index(g, w[0], w[1], w[2])] == 0;
+            }
+            if (ok) grid_dst[sg.dst_base + q * g.qs + ci] = v;
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
+                                 real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
+                                 const Geom &g, cudaStream_t s)
+{
+    if (nseg <= 0 || max_elems <= 0) return cudaSuccess;
+    int64_t bx = (max_elems + 255) / 256;
+    if (bx > 1024) bx = 1024;
+    for (int off = 0; off < nseg; off += 65535) {
+        int n = nseg - off < 65535 ? nseg - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n, 1);
+        copy_segments_kernel<real><<<grid, 256, 0, s>>>(segs + off, grid_src, grid_dst, buf_src, buf_dst, flags, g);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- flags
+__global__ void build_flags_kernel(const uint8_t *global, int64_t nx, int64_t ny, int64_t nz, int p0, int p1,
+                                   int p2, const int *origin, const Geom g, uint8_t *flags)
+{
+    const int lp = blockIdx.y;
+    const int64_t total = g.fs;
+    const int periodic[3] = {p0, p1, p2};
+    const int64_t n[3] = {nx, ny, nz};
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int col = (int)(e % g.px);
+        const int64_t r = e / g.px;
+        const int row = (int)(r % g.py);
+        const int pl = (int)(r / g.py);
+        const int lc[3] = {col - g.xo, row - 1, pl - 1};
+        uint8_t v = 1;
+        if (lc[0] >= -1 && lc[0] <= g.n[0]) {
+            int64_t c[3];
+            bool ok = true;
+            for (int ax = 0; ax < 3; ++ax) {
+                c[ax] = origin[3 * lp + ax] + lc[ax];
+                if (periodic[ax]) c[ax] = (c[ax] + n[ax]) % n[ax];
+                if (c[ax] < -1 || c[ax] > n[ax]) ok = false;
+            }
+            if (ok) v = global[((c[2] + 1) * (ny + 2) + (c[1] + 1)) * (nx + 2) + (c[0] + 1)];
+        }
+        flags[(int64_t)lp * g.fs + e] = v;
+    }
+}
+
+// kind: 2 = non-fluid (or ghost / padding), 1 = fluid with a non-fluid
+// neighbour among the 18 (needs the flag-driven path), 0 = fluid with only
+// fluid neighbours (pure pull).
+__global__ void build_kind_kernel(const Geom g, const uint8_t *flags, uint8_t *kind)
+{
+    const int lp = blockIdx.y;
+    const int64_t total = g.fs;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int col = (int)(e % g.px);
+        const int64_t r = e / g.px;
+        const int row = (int)(r % g.py);
+        const int pl = (int)(r / g.py);
+        const int x = col - g.xo, y = row - 1, z = pl - 1;
+        const uint8_t *f = flags + (int64_t)lp * g.fs;
+        uint8_t kd = 2;
+        if (x >= 0 && x < g.n[0] && y >= 0 && y < g.n[1] && z >= 0 && z < g.n[2] && f[e] == 0) {
+            kd = 0;
+            for (int i = 1; i < Q; ++i) {
+                const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+                if (f[e - sh] != 0) kd = 1;
+            }
+        }
+        kind[(int64_t)lp * g.fs + e] = kd;
+    }
+}
+
+cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], const int periodic[3],
+                               const int *patch_origin, int nlocal, const Geom &g, uint8_t *flags,
+                               uint8_t *kind, cudaStream_t s)
+{
+    int64_t bx = (g.fs + 255) / 256;
+    if (bx > 4096) bx = 4096;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n);
+        build_flags_kernel<<<grid, 256, 0, s>>>(global, domain[0], domain[1], domain[2], periodic[0], periodic[1],
+                                                periodic[2], patch_origin + 3 * off, g, flags + (int64_t)off * g.fs);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid((unsigned)bx, (unsigned)n);
+        build_kind_kernel<<<grid, 256, 0, s>>>(g, flags + (int64_t)off * g.fs, kind + (int64_t)off * g.fs);
+    }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- import / export
+struct OwnedMap {
+    int64_t lo[3];
+    int64_t n[3];
+    int brick[3];
+};
+
+__device__ __forceinline__ void owned_to_patch(const Geom &g, const int brick[3], int64_t ox, int64_t oy,
+                                               int64_t oz, int &lp, int &lx, int &ly, int &lz)
+{
+    const int bx = (int)(ox / g.n[0]), by = (int)(oy / g.n[1]), bz = (int)(oz / g.n[2]);
+    lx = (int)(ox - (int64_t)bx * g.n[0]);
+    ly = (int)(oy - (int64_t)by * g.n[1]);
+    lz = (int)(oz - (int64_t)bz * g.n[2]);
+    lp = (bz * brick[1] + by) * brick[0] + bx;
+}
+
+// rep: 0 = two-grid (slot i holds f_i), 1 = AA swapped (slot opp(i) holds f_i),
+//      2 = AA streamed (export only: f_i(x) = A[x + e_i][i], or at a wall
+//          x + e_i the bounced value A[x][opp(i)] minus its wall term).
+__device__ __forceinline__ int rep_slot(int rep, int i) { return rep == 1 ? OPP(i) : i; }
+
+template <typename real>
+__device__ __forceinline__ double read_state(const real *gp, const uint8_t *fp, const real *corr, const Geom &g,
+                                             int rep, int i)
+{
+    if (rep != 2) return (double)gp[rep_slot(rep, i) * g.qs];
+    const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+    const uint8_t f = fp[sh];
+    if (i == 0 || f == 0) return (double)gp[i * g.qs + sh];
+    real v = gp[OPP(i) * g.qs];
+    if (f >= 2) v -= corr[(f - 2) * Q + OPP(i)];
+    return (double)v;
+}
+
+template <typename real>
+__global__ void import_kernel(const double *canon, int64_t z0, int64_t ncells, int64_t nx, int64_t ny,
+                              int b0, int b1, int b2, const Geom g, real *grid, const int rep)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = z0 + r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) gp[rep_slot(rep, q) * g.qs] = (real)canon[c * Q + q];
+    }
+}
+
+template <typename real>
+__global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0, int64_t ncells, int64_t nx,
+                              int64_t ny, int b0, int b1, int b2, const Geom g, int mode, double *canon,
+                              double *rho, double *u, const int rep, const real *corr)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = z0 + r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        const int64_t ci = cell_index(g, lx, ly, lz);
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const bool fluid = fp[0] == 0;
+        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        if (mode == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+        } else {
+            // Macroscopic export: rho = rho0 + sum f~, u = sum e f~ / rho0.
+            double s = 0, jx = 0, jy = 0, jz = 0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const double v = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+                s += v;
+                jx += EX(q) * v;
+                jy += EY(q) * v;
+                jz += EZ(q) * v;
+            }
+            if (rho) rho[c] = fluid ? 1.0 + s : 0.0;
+            if (u) {
+                u[3 * c] = fluid ? jx : 0.0;
+                u[3 * c + 1] = fluid ? jy : 0.0;
+                u[3 * c + 2] = fluid ? jz : 0.0;
+            }
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_import(const double *canon, int64_t z0, int64_t nz_chunk, const int64_t owned_lo[3],
+                          const int64_t owned_n[3], const int brick[3], const Geom &g, real *grid, int rep,
+                          cudaStream_t s)
+{
+    (void)owned_lo;
+    const int64_t ncells = owned_n[0] * owned_n[1] * nz_chunk;
+    if (ncells <= 0) return cudaSuccess;
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 8192) nb = 8192;
+    import_kernel<real><<<(unsigned)nb, 256, 0, s>>>(canon, z0, ncells, owned_n[0], owned_n[1], brick[0],
+                                                    brick[1], brick[2], g, grid, rep);
+    return cudaGetLastError();
+}
+
+template <typename real>
+cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, int64_t nz_chunk,
+                          const int64_t owned_lo[3], const int64_t owned_n[3], const int brick[3],
+                          const Geom &g, double *canon, int mode, double *rho, double *u, int rep,
+                          const real *corr, cudaStream_t s)
+{
+    (void)owned_lo;
+    const int64_t ncells = owned_n[0] * owned_n[1] * nz_chunk;
+    if (ncells <= 0) return cudaSuccess;
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 8192) nb = 8192;
+    export_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, flags, z0, ncells, owned_n[0], owned_n[1], brick[0],
+                                                    brick[1], brick[2], g, mode, canon, rho, u, rep, corr);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- seeded noise (input generator)
+// Same counter-based generator as paper_1007_1388_b200/inputs.py (not part of
+// the method): k = splitmix64(global_index * 19 + q + seed * golden) % 2049 - 1024.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+template <typename real>
+__global__ void noise_kernel(real *grid, uint64_t seed, int64_t NX, int64_t NY, int64_t lox, int64_t loy,
+                             int64_t loz, int64_t nx, int64_t ny, int64_t ncells, int b0, int b1, int b2,
+                             const Geom g, const int rep)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        const uint64_t gi = (uint64_t)(((loz + oz) * NY + (loy + oy)) * NX + (lox + ox));
+        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const uint64_t key = gi * 19ull + (uint64_t)q + seed * 0x9E3779B97F4A7C15ull;
+            const int64_t k = (int64_t)(splitmix64(key) % 2049ull) - 1024;
+            gp[rep_slot(rep, q) * g.qs] = (real)((double)k * (1.0 / 1048576.0));
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_noise(real *grid, uint64_t seed, const int64_t domain[3], const int64_t owned_lo[3],
+                         const int64_t owned_n[3], const int brick[3], const Geom &g, int rep, cudaStream_t s)
+{
+    const int64_t ncells = owned_n[0] * owned_n[1] * owned_n[2];
+    int64_t nb = (ncells + 255) / 256;
+    if (nb > 16384) nb = 16384;
+    noise_kernel<real><<<(unsigned)nb, 256, 0, s>>>(grid, seed, domain[0], domain[1], owned_lo[0], owned_lo[1],
+                                                   owned_lo[2], owned_n[0], owned_n[1], ncells, brick[0], brick[1],
+                                                   brick[2], g, rep);
+    return cudaGetLastError();
+}
+
+template <typename real>
+__global__ void gather_kernel(const real *grid, const uint8_t *flags, const int64_t *xyz, int64_t n, int b0,
+                              int b1, int b2, const Geom g, double *out, const int rep, const real *corr)
+{
+    const int brick[3] = {b0, b1, b2};
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, xyz[3 * c], xyz[3 * c + 1], xyz[3 * c + 2], lp, lx, ly, lz);
+        const int64_t ci = cell_index(g, lx, ly, lz);
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const bool fluid = fp[0] == 0;
+        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+    }
+}
+
+template <typename real>
+cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t *xyz_local, int64_t n,
+                          const int brick[3], const Geom &g, double *out, int rep, const real *corr, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    int64_t nb = (n + 127) / 128;
+    if (nb > 4096) nb = 4096;
+    gather_kernel<real><<<(unsigned)nb, 128, 0, s>>>(grid, flags, xyz_local, n, brick[0], brick[1], brick[2], g, out,
+                                                     rep, corr);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- bounce-back fill
+// Writes, for the current state, the store-side bounce-back values of every
+// wall-adjacent fluid cell x into its wall neighbours: grid_opp(j)(x + e_j) =
+// grid_j(x) + corr.  Needed once after the state or the flags are set; every
+// later step maintains them inside the sweep.
+// aa = 0: two-grid state (wall slot opp(j) <- S_j(x)); aa = 1: AA swapped
+// state (S_j(x) = A[x][opp(j)], wall slot j, as the LOCAL kernel writes it).
+template <typename real>
+__global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr,
+                               const Geom g, const int aa)
+{
+    const int lp = blockIdx.y;
+    real *gp = grid + (int64_t)lp * g.ps;
+    const uint8_t *fp = flags + (int64_t)lp * g.fs;
+    const uint8_t *kp = kind + (int64_t)lp * g.fs;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.fs; e += (int64_t)gridDim.x * blockDim.x) {
+        if (kp[e] != 1) continue;
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            const uint8_t f = fp[e + sh];
+            if (f == 0) continue;
+            real v = gp[(aa ? OPP(j) : j) * g.qs + e];
+            if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
+            gp[(aa ? j : OPP(j)) * g.qs + e + sh] = v;
+        }
+    }
+}
+
+template <typename real>
+cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
+                           const Geom &g, int aa, cudaStream_t s)
+{
+    int64_t bx = (g.fs + 255) / 256;
+    if (bx > 2048) bx = 2048;
+    for (int off = 0; off < nlocal; off += 65535) {
+        int n = nlocal - off < 65535 ? nlocal - off : 65535;
+        dim3 grid_dim((unsigned)bx, (unsigned)n);
+        bb_fill_kernel<real><<<grid_dim, 256, 0, s>>>(grid + (int64_t)off * g.ps, flags + (int64_t)off * g.fs,
+                                                      kind + (int64_t)off * g.fs, corr, g, aa);
+    }
+    return cudaGetLastError();
+}
+
+#define LBM_INSTANTIATE(real)                                                                                   \
+    template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
+                                                    const real *, real *, const uint8_t *, const Geom &,       \
+                                                    cudaStream_t);                                             \
+    template cudaError_t launch_bb_fill<real>(real *, const uint8_t *, const uint8_t *, const real *, int,      \
+                                              const Geom &, int, cudaStream_t);                                \
+    template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
+                                             const int *, const Geom &, real *, int, cudaStream_t);            \
+    template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \
+                                             const int64_t *, const int *, const Geom &, double *, int,        \
+                                             double *, double *, int, const real *, cudaStream_t);             \
+    template cudaError_t launch_noise<real>(real *, uint64_t, const int64_t *, const int64_t *, const int64_t *, \
+                                            const int *, const Geom &, int, cudaStream_t);                     \
+    template cudaError_t launch_gather<real>(const real *, const uint8_t *, const int64_t *, int64_t,            \
+                                             const int *, const Geom &, double *, int, const real *,           \
+                                             cudaStream_t);
+
+LBM_INSTANTIATE(float)
+LBM_INSTANTIATE(double)
+
+}  // namespace lbm

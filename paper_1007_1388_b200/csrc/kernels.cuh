@@ -1,4 +1,4 @@
-// kernels.cuh -- launch wrappers of the sm_100a kernels (kernels.cu).
+// kernels.cuh -- launch wrappers of the sm_100a kernels (sweep.cu, sweep_aa.cu, aux_kernels.cu, sweep_direct.cu, sweep_tma.cu).
 #pragma once
 
 #include <cuda.h>
@@ -101,7 +101,7 @@ template <typename real>
 cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
                            const Geom &g, int aa, cudaStream_t s);
 
-// AA-pattern in-place sweeps (kernels.cu): pull = true -> PULL kernel, else LOCAL.
+// AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL.
 template <typename real>
 cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s);
 

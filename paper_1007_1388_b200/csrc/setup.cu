@@ -613,7 +613,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if ((v >= 0 && v < 8) || v >= 12) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
         if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
     }
-    if (const char *a = std::getenv("LBM_AA_VARIANT")) {  // AA kernels alone (12..15, kernels.cu launch_aa_x2)
+    if (const char *a = std::getenv("LBM_AA_VARIANT")) {  // AA kernels alone (12..15, sweep_aa.cu launch_aa_x2)
         int v = std::atoi(a);
         if ((v >= 0 && v < 8) || (v >= 12 && v < kSweepVariants)) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
     }

@@ -1,5 +1,5 @@
 // step.cu -- one time step (the paper's Sweep) on a rank: sweep
-// (fused pull + BB + collide, kernels.cu) and ghost exchange -- folded into the
+// (fused pull + BB + collide, sweep.cu / sweep_aa.cu) and ghost exchange -- folded into the
 // sweep as direct ghost stores (same GPU and, fused, NVLink stores into the
 // peers' grids with one epoch handshake), or extract -> NCCL -> insert
 // (P:287-313), shells first and overlapped with the interiors (the

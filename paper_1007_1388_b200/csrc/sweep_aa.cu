@@ -1,0 +1,315 @@
+// sweep_aa.cu -- AA-pattern in-place sweep kernels (one PDF array; north_star
+// (a)): the update of sweep.cu in alternating PULL /
+// LOCAL steps.
+#include <cstdint>
+
+#include "collide.cuh"
+#include "kernels.cuh"
+#include "sweep_common.cuh"
+
+namespace lbm {
+
+// ------------------------------------------------------------------ AA pattern
+// One PDF array, two alternating in-place kernels (north_star (a)).
+// With S_i(x) the post-collision state of the two-grid scheme:
+//   swapped  representation (after an even step count): A[x][opp(i)] = S_i(x)
+//   streamed representation (after an odd step count):  A[x][i] = p_i(x), the
+//                                                        value x pulls next
+// PULL  (swapped -> streamed): p_i = A[x - e_i][opp(i)]; collide; write out_i to
+//       A[x + e_i][i], or -- x + e_i a wall -- its bounce-back
+//       out_i + 6 w rho0 e_opp(i).u_w to A[x][opp(i)] (R3).
+// LOCAL (streamed -> swapped): p_i = A[x][i]; collide; A[x][opp(i)] = out_i, and
+//       for walls w = x + e_j the store-side bounce-back A[w][j] = out_j + corr,
+//       which the next PULL gathers branch-free.
+// Every slot has exactly one writer per step and is read only by it, so both
+// kernels run in place without races; the results equal the two-grid scheme
+// bitwise after every even step count.
+template <typename real, bool PULL, int MINB, int STCS>
+__global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(const SweepArgs<real> a)
+{
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    const int x = bx.lo[0] + tx * SWEEP_BX + (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    if (x >= bx.lo[0] + bx.n[0] || y >= bx.lo[1] + bx.n[1]) return;
+
+    const Geom &g = a.g;
+    const int64_t qs = g.qs;
+    const int64_t cell = cell_index(g, x, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k = a.kind[fbase];
+    real *A = a.dst + pbase;  // in place: src == dst
+    real p[Q];
+    if (PULL) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            p[i] = ld_stream((const real *)A + OPP(i) * qs - sh);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) p[i] = ld_stream((const real *)A + i * qs);
+    }
+    if (k == 2) return;
+    uint8_t nbf[Q];
+    if (k == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            nbf[j] = a.flags[fbase + sh];  // flag of x + e_j
+        }
+    }
+    collide_bgk<real>(p, a.omega);
+    if (PULL) {
+        st_stream<real, STCS>(A, p[0]);
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            if (k == 1 && nbf[i] != 0) {
+                real v = p[i];
+                if (nbf[i] >= 2) v += a.corr[(nbf[i] - 2) * Q + OPP(i)];
+                A[OPP(i) * qs] = v;
+            } else {
+                st_stream<real, STCS>(A + i * qs + sh, p[i]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) st_stream<real, STCS>(A + OPP(i) * qs, p[i]);
+        if (k == 1) {
+#pragma unroll
+            for (int j = 1; j < Q; ++j) {
+                if (nbf[j] != 0) {
+                    const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                    real v = p[j];
+                    if (nbf[j] >= 2) v += a.corr[(nbf[j] - 2) * Q + OPP(j)];
+                    A[j * qs + sh] = v;
+                }
+            }
+        }
+    }
+}
+
+// AA-pattern kernels with two cells per thread along x (cf. sweep_x2_kernel):
+// LOCAL reads and writes only its own cells, so all 19 loads and 19 stores are
+// aligned 2-vectors; PULL vectorises the 9 gathers and scatters with e_x = 0.
+// A pair whose cells differ in kind (non-fluid, or a bounce-back redirect for
+// that direction) falls back to scalar accesses.  Pairs with no wall next to
+// either cell (kind 0, the common case) take a straight-line store path: the
+// per-direction redirect tests cost PULL +41 % instructions over the two-grid
+// sweep in this latency-bound kernel (1.05 -> 0.88 ms at 256^3 fp64,
+// profiles/r01_ncu_aa_*).  Realigning the 10 e_x != 0 scatters into 2-vectors
+// with warp shuffles was measured slower (tools/stream_ceiling.cu mode 3: the
+// ceiling gains 1.6 %, the kernel loses more to the shuffles).
+template <typename real, bool PULL, int MINB>
+__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const SweepArgs<real> a)
+{
+    using V2 = typename Vec2<real>::T;
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    const int x0 = bx.lo[0] + tx * SWEEP_BX + 2 * (int)threadIdx.x;
+    const int y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    const int z = bx.lo[2] + tz;
+    const int xend = bx.lo[0] + bx.n[0];
+    if (x0 >= xend || y >= bx.lo[1] + bx.n[1]) return;
+    const bool has1 = x0 + 1 < xend;
+
+    const Geom &g = a.g;
+    const int64_t qs = g.qs;
+    const int64_t cell = cell_index(g, x0, y, z);
+    const int64_t pbase = (int64_t)bx.patch * g.ps + cell;
+    const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
+    const uint8_t k0 = a.kind[fbase];
+    const uint8_t k1 = has1 ? a.kind[fbase + 1] : (uint8_t)2;
+    real *A = a.dst + pbase;  // in place
+    real p0[Q], p1[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        if (PULL) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            const real *src = A + OPP(i) * qs - sh;
+            if (EX(i) == 0) {
+                const V2 v = __ldg(reinterpret_cast<const V2 *>(src));
+                p0[i] = v.x;
+                p1[i] = v.y;
+            } else {
+                p0[i] = __ldg(src);
+                p1[i] = __ldg(src + 1);
+            }
+        } else {
+            const V2 v = __ldg(reinterpret_cast<const V2 *>(A + i * qs));
+            p0[i] = v.x;
+            p1[i] = v.y;
+        }
+    }
+    if (k0 == 2 && k1 == 2) return;
+    uint8_t f0[Q], f1[Q];
+#pragma unroll
+    for (int j = 0; j < Q; ++j) f0[j] = f1[j] = 0;
+    if (k0 == 1 || k1 == 1) {
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            if (k0 == 1) f0[j] = a.flags[fbase + sh];
+            if (k1 == 1) f1[j] = a.flags[fbase + 1 + sh];
+        }
+    }
+    collide_bgk<real>(p0, a.omega);
+    collide_bgk<real>(p1, a.omega);
+    const bool both = k0 != 2 && k1 != 2;
+    if (PULL && k0 == 0 && k1 == 0) {
+        // no wall next to either cell (the common case): straight-line scatter
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            if (EX(i) == 0) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + i * qs + sh) = w;
+            } else {
+                A[i * qs + sh] = p0[i];
+                A[i * qs + sh + 1] = p1[i];
+            }
+        }
+    } else if (PULL) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
+            const bool r0 = f0[i] != 0, r1 = f1[i] != 0;  // x + e_i is a wall: bounce back into x
+            if (EX(i) == 0 && both && !r0 && !r1) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + i * qs + sh) = w;
+                continue;
+            }
+            if (k0 != 2) {
+                if (r0) {
+                    real v = p0[i];
+                    if (f0[i] >= 2) v += a.corr[(f0[i] - 2) * Q + OPP(i)];
+                    A[OPP(i) * qs] = v;
+                } else {
+                    A[i * qs + sh] = p0[i];
+                }
+            }
+            if (k1 != 2) {
+                if (r1) {
+                    real v = p1[i];
+                    if (f1[i] >= 2) v += a.corr[(f1[i] - 2) * Q + OPP(i)];
+                    A[OPP(i) * qs + 1] = v;
+                } else {
+                    A[i * qs + sh + 1] = p1[i];
+                }
+            }
+        }
+    } else {
+        if (both) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                V2 w;
+                w.x = p0[i];
+                w.y = p1[i];
+                *reinterpret_cast<V2 *>(A + OPP(i) * qs) = w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+                if (k0 != 2) A[OPP(i) * qs] = p0[i];
+                if (k1 != 2) A[OPP(i) * qs + 1] = p1[i];
+            }
+        }
+        if (k0 != 1 && k1 != 1) return;
+        // store-side bounce-back into wall slots (see sweep_aa_kernel)
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+            if (f0[j] != 0) {
+                real v = p0[j];
+                if (f0[j] >= 2) v += a.corr[(f0[j] - 2) * Q + OPP(j)];
+                A[j * qs + sh] = v;
+            }
+            if (f1[j] != 0) {
+                real v = p1[j];
+                if (f1[j] >= 2) v += a.corr[(f1[j] - 2) * Q + OPP(j)];
+                A[j * qs + sh + 1] = v;
+            }
+        }
+    }
+}
+
+template <typename real>
+static void launch_aa_x2(const SweepArgs<real> &a, unsigned grid, bool pull, int variant, cudaStream_t s)
+{
+    dim3 block(32, SWEEP_BY, 1);
+    constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
+    // 12 / 14: min blocks M0; 13 / 15: M1
+    const bool m1 = variant == 13 || variant == 15;
+    if (pull) {
+        if (m1) sweep_aa_x2_kernel<real, true, M1><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, true, M0><<<grid, block, 0, s>>>(a);
+    } else {
+        if (m1) sweep_aa_x2_kernel<real, false, M1><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, false, M0><<<grid, block, 0, s>>>(a);
+    }
+}
+
+template <typename real>
+cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s)
+{
+    if (total_tiles <= 0) return cudaSuccess;
+    dim3 block(SWEEP_BX, SWEEP_BY, 1);
+    const unsigned grid = (unsigned)total_tiles;
+    if (variant >= 12) {
+        launch_aa_x2<real>(a, grid, pull, variant, s);
+        return cudaGetLastError();
+    }
+    const int v = variant & 7;  // min blocks / store hint as for the two-grid sweep
+    if (pull) {
+        switch (v) {
+        case 4: sweep_aa_kernel<real, true, 3, 0><<<grid, block, 0, s>>>(a); break;
+        case 5: sweep_aa_kernel<real, true, 3, 1><<<grid, block, 0, s>>>(a); break;
+        case 6: sweep_aa_kernel<real, true, 4, 0><<<grid, block, 0, s>>>(a); break;
+        case 7: sweep_aa_kernel<real, true, 4, 1><<<grid, block, 0, s>>>(a); break;
+        default: sweep_aa_kernel<real, true, 2, 0><<<grid, block, 0, s>>>(a); break;
+        }
+    } else {
+        switch (v) {
+        case 4: sweep_aa_kernel<real, false, 3, 0><<<grid, block, 0, s>>>(a); break;
+        case 5: sweep_aa_kernel<real, false, 3, 1><<<grid, block, 0, s>>>(a); break;
+        case 6: sweep_aa_kernel<real, false, 4, 0><<<grid, block, 0, s>>>(a); break;
+        case 7: sweep_aa_kernel<real, false, 4, 1><<<grid, block, 0, s>>>(a); break;
+        default: sweep_aa_kernel<real, false, 2, 0><<<grid, block, 0, s>>>(a); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
+template cudaError_t launch_sweep_aa<float>(const SweepArgs<float> &, int64_t, bool, int, cudaStream_t);
+template cudaError_t launch_sweep_aa<double>(const SweepArgs<double> &, int64_t, bool, int, cudaStream_t);
+
+}  // namespace lbm

@@ -1,8 +1,8 @@
 // sweep_tma.cu -- TMA-staged, warp-specialised persistent sweep (sm_100a).
 //
-// Same update as sweep_kernel (kernels.cu): branch-free pull +
+// Same update as sweep_kernel (sweep.cu): branch-free pull +
 // BGK collide (eq:lbm / eq:feq) on centred PDFs, with
-// half-way bounce-back applied on the store side (see kernels.cu).
+// half-way bounce-back applied on the store side (see sweep.cu).
 // What differs is how the pull neighbourhood reaches the SM: the pull of
 // direction i for a tile of TX x TY cells of one z-plane is the TX x TY box of
 // q-slice i shifted by -e_i, so a producer warp issues 19

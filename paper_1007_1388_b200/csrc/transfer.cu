@@ -52,7 +52,7 @@ lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode,
     if (zc < 1) zc = 1;
     if (zc > on[2]) zc = on[2];
     const void *grid = ctx->grid[ctx->cur];
-    // representation of the state in the grid (kernels.cu rep_slot / read_state)
+    // representation of the state in the grid (aux_kernels.cu rep_slot / read_state)
     const int rep = ctx->layout == LBM_LAYOUT_AA ? (to_device || ctx->aa_phase == 0 ? 1 : 2) : 0;
     if (to_device) ctx->aa_phase = 0;
     cudaStream_t cs = ctx->stream, xs = ctx->xstream;
