@@ -502,8 +502,10 @@ lbm_status setup_direct(lbm_ctx *ctx)
         // all-gather {grid0, grid1, inbox} IPC handles
         const size_t hb = sizeof(cudaIpcMemHandle_t);
         std::vector<cudaIpcMemHandle_t> mine(3);
+        // the AA layout has one grid: its handle travels in both slots, opened once
+        const bool aa = ctx->layout == LBM_LAYOUT_AA;
         CK(cudaIpcGetMemHandle(&mine[0], ctx->grid[0]));
-        CK(cudaIpcGetMemHandle(&mine[1], ctx->grid[1]));
+        CK(cudaIpcGetMemHandle(&mine[1], ctx->grid[aa ? 0 : 1]));
         CK(cudaIpcGetMemHandle(&mine[2], ctx->d_inbox));
         char *dbuf = nullptr;
         if ((st = dev_alloc(ctx, &dbuf, 3 * hb * (size_t)(R + 1)))) return st;
@@ -517,6 +519,10 @@ lbm_status setup_direct(lbm_ctx *ctx)
         int ok = 1;
         for (int r : peers) {
             for (int i = 0; i < 3 && ok; ++i) {
+                if (aa && i == 1) {
+                    peer_grid[(size_t)2 * r + 1] = peer_grid[(size_t)2 * r];
+                    continue;
+                }
                 void *ptr = nullptr;
                 if (cudaIpcOpenMemHandle(&ptr, all[(size_t)3 * r + i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                     cudaGetLastError();
@@ -758,12 +764,20 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             return bail(LBM_ERR_NCCL);
         }
     }
+    // The x2 sweeps (two-grid: sweep.cu, AA: sweep_aa.cu) can store the outgoing
+    // PDFs of face cells straight into neighbour patches (direct ghost stores).
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    const bool x2 = !ctx->use_tma && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
+                    (aa ? ctx->aa_variant[ctx->esize == 8 ? 1 : 0] : ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]) >= 12;
+    const char *e_shell = std::getenv("LBM_SHELL_KERNEL");
+    const bool onecell = e_shell && std::string(e_shell) == "onecell";
     {
-        // Fused exchange for the two-grid layout unless the NCCL path is requested
-        // (exchange_mode FORCE_BUFFERS, or env LBM_EXCHANGE=nccl).
+        // Fused exchange across GPUs unless the NCCL path is requested (exchange_mode
+        // FORCE_BUFFERS, or env LBM_EXCHANGE=nccl); the AA layout needs the x2 kernels
+        // (its shells have no one-cell fused kernel).
         const char *ev = std::getenv("LBM_EXCHANGE");
-        const bool want = ctx->layout == LBM_LAYOUT_AB && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
-                          !(ev && std::string(ev) == "nccl");
+        const bool want = cfg->exchange_mode == LBM_EXCHANGE_AUTO && !(ev && std::string(ev) == "nccl") &&
+                          (!aa || (x2 && !onecell));
         if (want && (st = setup_direct(ctx))) return bail(st);
     }
     {
@@ -801,13 +815,9 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         //     the same kernel through the peer-mapped table instead of the
         //     one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell keeps it).
         const char *ev = std::getenv("LBM_LOCAL_DIRECT");
-        const char *es = std::getenv("LBM_SHELL_KERNEL");
-        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
-        const bool x2 = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
-                        v >= 12;
         const bool want_local = x2 && !ctx->lpull && !(ev && std::string(ev) == "0") &&
                                 !ctx->ex[EX_AB].segs.local.empty();
-        const bool want_shell = x2 && ctx->direct && !(es && std::string(es) == "onecell");
+        const bool want_shell = x2 && ctx->direct && !onecell;
         if (want_local || want_shell) {
             std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);
             for (int l = 0; l < dec.nlocal && want_local; ++l) {
@@ -816,7 +826,8 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
                     const int nbp = neighbour(dec, gp, kDirs[k].d);
                     if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
                     const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
-                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
+                    for (int i = 0; i < 2; ++i)  // AA: one grid
+                        tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[aa ? 0 : i] + off;
                 }
             }
             if ((st = dev_alloc(ctx, &ctx->d_dnbr, tab.size() * sizeof(void *)))) return bail(st);

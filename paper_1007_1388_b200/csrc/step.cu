@@ -34,8 +34,8 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.nboxes = b.n;
     a.lnbr = ctx->lpull ? (const real *const *)ctx->d_lnbr : nullptr;
     a.srci = ctx->cur;
-    a.dnbr = ctx->ldirect && ctx->layout == LBM_LAYOUT_AB ? (real *const *)ctx->d_dnbr : nullptr;
-    a.dsti = 1 - ctx->cur;
+    a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
+    a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
     return a;
 }
 
@@ -234,14 +234,17 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         ctx->launches += 1;
         const DevBoxes &bs = ctx->box_shell;
         if (bs.tiles > 0 && ctx->x2_shells) {
+            const bool pull = ctx->aa_phase == 0;  // AA: PULL after an even step count
             if (ctx->esize == 8) {
                 SweepArgs<double> a = sweep_args<double>(ctx, bs);
                 a.dnbr = (double *const *)ctx->d_dnbr;
-                e = launch_sweep<double>(a, bs.tiles, ctx->sweep_variant[1], c);
+                e = aa ? launch_sweep_aa<double>(a, bs.tiles, pull, ctx->aa_variant[1], c)
+                       : launch_sweep<double>(a, bs.tiles, ctx->sweep_variant[1], c);
             } else {
                 SweepArgs<float> a = sweep_args<float>(ctx, bs);
                 a.dnbr = (float *const *)ctx->d_dnbr;
-                e = launch_sweep<float>(a, bs.tiles, ctx->sweep_variant[0], c);
+                e = aa ? launch_sweep_aa<float>(a, bs.tiles, pull, ctx->aa_variant[0], c)
+                       : launch_sweep<float>(a, bs.tiles, ctx->sweep_variant[0], c);
             }
             if (e != cudaSuccess) return ctx->cuda_fail(e, "shell sweep launch", __FILE__, __LINE__);
             ctx->launches += 1;

@@ -114,7 +114,92 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(cons
 // profiles/r01_ncu_aa_*).  Realigning the 10 e_x != 0 scatters into 2-vectors
 // with warp shuffles was measured slower (tools/stream_ceiling.cu mode 3: the
 // ceiling gains 1.6 %, the kernel loses more to the shuffles).
-template <typename real, bool PULL, int MINB>
+// ------------------------------------------------- direct ghost stores (AA)
+// The AA pattern's two half-exchanges folded into the
+// sweep, as sweep.cu does for the two-grid layout:
+//   LOCAL: a fluid cell g on a patch face / edge stores out_q, for each q that
+//          travels into the neighbour, into the neighbour's ghost copy of g at
+//          slot opp(q) -- what the neighbour's next PULL gathers there;
+//   PULL:  a fluid cell x whose scatter target x + e_q lies in a neighbour patch
+//          (and is fluid) stores out_q into that cell of the neighbour, slot q --
+//          what the neighbour's next LOCAL reads.  Only fluid writers store:
+//          the writer mask of half-exchange 2 holds by construction.
+// Every slot keeps exactly one writer per step, so this races with nothing.
+
+// (oz, oy, ox) + 1 in base 3 -> neighbour direction kd of the plan order, -1: none
+__constant__ int8_t c_kd27[27] = {-1, 0,  -1, 1,  2,  3,  -1, 4,  -1, 5,  6,  7,  8, -1,
+                                  9,  10, 11, 12, -1, 13, -1, 14, 15, 16, -1, 17, -1};
+
+template <typename real>
+__device__ __forceinline__ real *aa_nbr(const SweepArgs<real> &a, int patch, int kd)
+{
+    return (real *)__ldg(reinterpret_cast<const unsigned long long *>(a.dnbr + ((int64_t)patch * NDIR + kd) * 2));
+}
+
+template <typename real>
+__device__ __forceinline__ void aa_local_direct(const SweepArgs<real> &a, int patch, int x, int y, int z,
+                                                const real *p)
+{
+    const Geom &g = a.g;
+    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+#pragma unroll
+    for (int kd = 0; kd < NDIR; ++kd) {
+        const int ddx = ndir(kd, 0), ddy = ndir(kd, 1), ddz = ndir(kd, 2);
+        const bool on = (ddx == 0 || (ddx > 0 ? x == n0 - 1 : x == 0)) &&
+                        (ddy == 0 || (ddy > 0 ? y == n1 - 1 : y == 0)) &&
+                        (ddz == 0 || (ddz > 0 ? z == n2 - 1 : z == 0));
+        if (!on) continue;
+        real *nb = aa_nbr(a, patch, kd);
+        if (!nb) continue;
+        real *gc = nb + cell_index(g, x - ddx * n0, y - ddy * n1, z - ddz * n2);
+#pragma unroll
+        for (int q = 1; q < Q; ++q)
+            if (outgoing(q, kd)) gc[OPP(q) * g.qs] = p[q];
+    }
+}
+
+template <typename real>
+__device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int patch, int x, int y, int z, uint8_t k,
+                                               const uint8_t *f, const real *p)
+{
+    const Geom &g = a.g;
+    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        const int dx = x + EX(q), dy = y + EY(q), dz = z + EZ(q);
+        const int ox = dx < 0 ? -1 : (dx >= n0 ? 1 : 0);
+        const int oy = dy < 0 ? -1 : (dy >= n1 ? 1 : 0);
+        const int oz = dz < 0 ? -1 : (dz >= n2 ? 1 : 0);
+        if ((ox | oy | oz) == 0) continue;   // target inside the patch
+        if (k == 1 && f[q] != 0) continue;   // wall target: the bounce-back stays at x
+        const int kd = c_kd27[(oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)];
+        real *nb = aa_nbr(a, patch, kd);
+        if (!nb) continue;
+        nb[q * g.qs + cell_index(g, dx - ox * n0, dy - oy * n1, dz - oz * n2)] = p[q];
+    }
+}
+
+// A pair (x0, x0 + 1): only cells on a patch face do anything.
+template <typename real, bool PULL>
+__device__ __forceinline__ void aa_direct_pair(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool has1,
+                                               uint8_t k0, uint8_t k1, const uint8_t *f0, const uint8_t *f1,
+                                               const real *p0, const real *p1)
+{
+    const Geom &g = a.g;
+    const bool yzf = y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1;  // warp-uniform
+    const bool c0 = k0 != 2 && (yzf || x0 == 0 || x0 == g.n[0] - 1);
+    const bool c1 = has1 && k1 != 2 && (yzf || x0 + 1 == g.n[0] - 1);
+    if (c0) {
+        if (PULL) aa_pull_direct<real>(a, patch, x0, y, z, k0, f0, p0);
+        else aa_local_direct<real>(a, patch, x0, y, z, p0);
+    }
+    if (c1) {
+        if (PULL) aa_pull_direct<real>(a, patch, x0 + 1, y, z, k1, f1, p1);
+        else aa_local_direct<real>(a, patch, x0 + 1, y, z, p1);
+    }
+}
+
+template <typename real, bool PULL, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const SweepArgs<real> a)
 {
     using V2 = typename Vec2<real>::T;
@@ -243,23 +328,25 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
                 if (k1 != 2) A[OPP(i) * qs + 1] = p1[i];
             }
         }
-        if (k0 != 1 && k1 != 1) return;
-        // store-side bounce-back into wall slots (see sweep_aa_kernel)
+        if (k0 == 1 || k1 == 1) {
+            // store-side bounce-back into wall slots (see sweep_aa_kernel)
 #pragma unroll
-        for (int j = 1; j < Q; ++j) {
-            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-            if (f0[j] != 0) {
-                real v = p0[j];
-                if (f0[j] >= 2) v += a.corr[(f0[j] - 2) * Q + OPP(j)];
-                A[j * qs + sh] = v;
-            }
-            if (f1[j] != 0) {
-                real v = p1[j];
-                if (f1[j] >= 2) v += a.corr[(f1[j] - 2) * Q + OPP(j)];
-                A[j * qs + sh + 1] = v;
+            for (int j = 1; j < Q; ++j) {
+                const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
+                if (f0[j] != 0) {
+                    real v = p0[j];
+                    if (f0[j] >= 2) v += a.corr[(f0[j] - 2) * Q + OPP(j)];
+                    A[j * qs + sh] = v;
+                }
+                if (f1[j] != 0) {
+                    real v = p1[j];
+                    if (f1[j] >= 2) v += a.corr[(f1[j] - 2) * Q + OPP(j)];
+                    A[j * qs + sh + 1] = v;
+                }
             }
         }
     }
+    if (DIRECT) aa_direct_pair<real, PULL>(a, bx.patch, x0, y, z, has1, k0, k1, f0, f1, p0, p1);
 }
 
 template <typename real>
@@ -267,14 +354,24 @@ static void launch_aa_x2(const SweepArgs<real> &a, unsigned grid, bool pull, int
 {
     dim3 block(32, SWEEP_BY, 1);
     constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
-    // 12 / 14: min blocks M0; 13 / 15: M1
+    // 12 / 14: min blocks M0; 13 / 15: M1; a.dnbr: with direct ghost stores
     const bool m1 = variant == 13 || variant == 15;
+    if (a.dnbr) {
+        if (pull) {
+            if (m1) sweep_aa_x2_kernel<real, true, M1, true><<<grid, block, 0, s>>>(a);
+            else sweep_aa_x2_kernel<real, true, M0, true><<<grid, block, 0, s>>>(a);
+        } else {
+            if (m1) sweep_aa_x2_kernel<real, false, M1, true><<<grid, block, 0, s>>>(a);
+            else sweep_aa_x2_kernel<real, false, M0, true><<<grid, block, 0, s>>>(a);
+        }
+        return;
+    }
     if (pull) {
-        if (m1) sweep_aa_x2_kernel<real, true, M1><<<grid, block, 0, s>>>(a);
-        else sweep_aa_x2_kernel<real, true, M0><<<grid, block, 0, s>>>(a);
+        if (m1) sweep_aa_x2_kernel<real, true, M1, false><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, true, M0, false><<<grid, block, 0, s>>>(a);
     } else {
-        if (m1) sweep_aa_x2_kernel<real, false, M1><<<grid, block, 0, s>>>(a);
-        else sweep_aa_x2_kernel<real, false, M0><<<grid, block, 0, s>>>(a);
+        if (m1) sweep_aa_x2_kernel<real, false, M1, false><<<grid, block, 0, s>>>(a);
+        else sweep_aa_x2_kernel<real, false, M0, false><<<grid, block, 0, s>>>(a);
     }
 }
 

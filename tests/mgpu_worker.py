@@ -38,11 +38,12 @@ def main():
     # shells swept by the one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell)
     combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "fused_copies", grids[0]),
               (4, 1, 0, "fused_onecell", grids[0]),
-              (8, 1, 0, "nccl", grids[0]),
+              (8, 1, 0, "nccl", grids[0]), (8, 1, 1, "fused", grids[0]), (4, 1, 1, "fused", grids[0]),
               (8, 0, 0, "nccl", grids[0]), (4, 1, 0, "nccl", grids[0]), (8, 1, 1, "nccl", grids[0]),
               (4, 0, 1, "nccl", grids[0])]
     for pg in grids[1:]:
-        combos += [(8, 1, 0, "fused", pg), (4, 1, 0, "fused", pg), (8, 1, 0, "nccl", pg), (8, 1, 1, "nccl", pg)]
+        combos += [(8, 1, 0, "fused", pg), (4, 1, 0, "fused", pg), (8, 1, 0, "nccl", pg), (8, 1, 1, "nccl", pg),
+                   (8, 1, 1, "fused", pg)]
     for prec, overlap, layout, exch, pgrid in combos:
         if exch == "nccl":
             os.environ["LBM_EXCHANGE"] = "nccl"
@@ -76,8 +77,8 @@ def main():
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
                 results[(prec, overlap, layout, exch, tuple(pgrid))] = full
                 assert info["exchange_fused"] == (1 if exch.startswith("fused") else 0), info["exchange_fused"]
-                # 8+ patches per rank: same-GPU neighbours take the direct ghost stores (AB)
-                assert info["local_direct"] == (1 if layout == 0 and exch != "fused_copies" else 0), info
+                # 8+ patches per rank: same-GPU neighbours take the direct ghost stores
+                assert info["local_direct"] == (0 if exch == "fused_copies" else 1), info
                 print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} peers={info['peers']} "
                       f"halo={info['halo_bytes_remote_per_step']} local_direct={info['local_direct']}", flush=True)
     if rank == 0:

@@ -156,3 +156,33 @@ def test_aa_variants_bitwise(prec, n, patch, monkeypatch):
     ab = run(n, fl, wu, f0, 10, prec, m.LBM_LAYOUT_AB, patch=patch, periodic=(0, 1, 0))[0]
     for v in ("12", "13"):
         np.testing.assert_array_equal(out[v], ab)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("n,patch,periodic", [((64, 30, 24), (16, 10, 12), (1, 0, 1)),
+                                              ((60, 30, 24), (15, 30, 8), (1, 1, 0)),
+                                              ((6, 4, 6), (1, 1, 2), (1, 1, 1))])
+def test_aa_direct_stores_equal_half_exchanges(prec, n, patch, periodic, monkeypatch):
+    """AA layout, many patches on one GPU: the sweep's direct stores (LOCAL: own
+    cell into the neighbour's ghost, slot opp(q); PULL: scatter target in the
+    neighbour, slot q) give bitwise the half-exchange copies and the two-grid
+    layout, at even and odd step counts (odd: un-streamed export)."""
+    m = lbm()
+    fl, wu = inputs.ldc_flags(n, periodic=periodic)
+    fl = inputs.add_obstacles(fl, 0.06, seed=47, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.0, 0.01, 0.02]]])
+    f0 = inputs.noise_pdfs(n, seed=53)
+    for steps in (4, 7):
+        out = {}
+        for ld in ("1", "0"):
+            monkeypatch.setenv("LBM_LOCAL_DIRECT", ld)
+            aa, rho, _, info = run(n, fl, wu, f0, steps, prec, m.LBM_LAYOUT_AA, patch=patch, periodic=periodic)
+            assert info["local_direct"] == int(ld)
+            out[ld] = aa
+        np.testing.assert_array_equal(out["1"], out["0"])
+        monkeypatch.delenv("LBM_LOCAL_DIRECT")
+        ab = run(n, fl, wu, f0, steps, prec, m.LBM_LAYOUT_AB, patch=patch, periodic=periodic)[0]
+        if steps % 2 == 0:
+            np.testing.assert_array_equal(out["1"], ab)
+        else:
+            assert np.abs(out["1"] - ab).max() <= ODD_TOL_VS_AB[prec]
