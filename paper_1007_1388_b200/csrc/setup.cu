@@ -814,9 +814,14 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         // (2) with the fused exchange, the shells facing other GPUs are swept by
         //     the same kernel through the peer-mapped table instead of the
         //     one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell keeps it).
+        // AA default: only for small patches -- the AA direct kernels spill, which
+        // costs 3.8 % of the sweep at 384^3 (more than the ghost copies), while at
+        // 64^3 the copies cost more; LBM_LOCAL_DIRECT=1 / 0 forces it.
         const char *ev = std::getenv("LBM_LOCAL_DIRECT");
-        const bool want_local = x2 && !ctx->lpull && !(ev && std::string(ev) == "0") &&
-                                !ctx->ex[EX_AB].segs.local.empty();
+        const int pmin = std::min(ctx->g.n[0], std::min(ctx->g.n[1], ctx->g.n[2]));
+        const bool dflt = !aa || pmin <= 128;
+        const bool on = ev ? std::string(ev) != "0" : dflt;
+        const bool want_local = x2 && !ctx->lpull && on && !ctx->ex[EX_AB].segs.local.empty();
         const bool want_shell = x2 && ctx->direct && !onecell;
         if (want_local || want_shell) {
             std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);

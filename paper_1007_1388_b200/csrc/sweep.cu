@@ -16,6 +16,7 @@
 
 #include "collide.cuh"
 #include "kernels.cuh"
+#include "direct_stores.cuh"
 #include "sweep_common.cuh"
 
 namespace lbm {
@@ -111,138 +112,6 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
 // scalars: a wall cell's slots hold store-side bounce-back values of its
 // neighbours and must not be overwritten.  Block (32, 4) threads = 64 x 4 cells.
 
-// Direct ghost stores of a cell pair (x0, x0 + 1) -- the pack / copy / unpack of
-// P:331-337 folded into the sweep: a fluid cell on a patch face or edge stores
-// each PDF that travels into the neighbour at d (5 per face, 1 per edge) into
-// that neighbour's ghost cell at the same global position, in the grid the
-// neighbour pulls from next step.  c0 / c1: the cell is fluid and in the box.
-// A ghost column (x = -1, or x = n when sector-aligned) shares its 32-B sector
-// only with row padding, which nothing reads: storing the whole sector (value +
-// zeros) spares L2 the DRAM fill of a partially written sector -- strided
-// 4 / 8-B column stores otherwise cost a read-modify-write each.
-template <typename real>
-__device__ __forceinline__ void st_ghost_sector(real *sector, bool last, real v)
-{
-    if constexpr (sizeof(real) == 4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (last) b.w = v; else a.x = v;
-        reinterpret_cast<float4 *>(sector)[0] = a;
-        reinterpret_cast<float4 *>(sector)[1] = b;
-    } else {
-        double2 a = make_double2(0.0, 0.0), b = a;
-        if (last) b.y = v; else a.x = v;
-        reinterpret_cast<double2 *>(sector)[0] = a;
-        reinterpret_cast<double2 *>(sector)[1] = b;
-    }
-}
-
-// Direct stores toward neighbour kd (compile-time after unrolling) of a cell
-// pair whose cells are on that side (on0 / on1).
-template <typename real>
-__device__ __forceinline__ real *direct_ptr(const SweepArgs<real> &a, int patch, int kd)
-{
-    return (real *)__ldg(reinterpret_cast<const unsigned long long *>(a.dnbr + ((int64_t)patch * NDIR + kd) * 2 +
-                                                                      a.dsti));
-}
-
-template <typename real, int KD>
-__device__ __forceinline__ void direct_dir_x2(const SweepArgs<real> &a, real *nb, int x0, int y, int z, bool on0,
-                                              bool on1, const real *p0, const real *p1)
-{
-    using V2 = typename Vec2<real>::T;
-    constexpr int ddx = ndir(KD, 0), ddy = ndir(KD, 1), ddz = ndir(KD, 2);
-    if ((!on0 && !on1) || !nb) return;
-    const Geom &g = a.g;
-    const int64_t qs = g.qs;
-    const int n0 = g.n[0];
-    real *gb = nb + cell_index(g, x0 - ddx * n0, y - ddy * g.n[1], z - ddz * g.n[2]);
-    if constexpr (ddx != 0) {
-        constexpr int SE = 32 / (int)sizeof(real);  // elements per 32-B sector
-        // ghost column x = -1 (ddx > 0) ends a sector; x = n0 (ddx < 0) may start one
-        const bool whole = ddx > 0 ? (g.xo >= SE && g.xo % SE == 0)
-                                   : ((g.xo + n0) % SE == 0 && g.xo + n0 + SE <= g.px);
-        if (whole) {
-            // exactly one cell of the pair lies on the x face (x0 == 0 for ddx < 0;
-            // x0 or x0 + 1 == n0 - 1 for ddx > 0)
-            const real *pv = on0 ? p0 : p1;
-            real *gs = gb + (on0 ? 0 : 1) - (ddx > 0 ? SE - 1 : 0);
-#pragma unroll
-            for (int q = 1; q < Q; ++q)
-                if (outgoing(q, KD)) st_ghost_sector<real>(gs + q * qs, ddx > 0, pv[q]);
-            return;
-        }
-    }
-#pragma unroll
-    for (int q = 1; q < Q; ++q) {
-        if (!outgoing(q, KD)) continue;
-        if (ddx == 0 && on0 && on1) {  // same x as the pair: aligned 2-vector
-            V2 w;
-            w.x = p0[q];
-            w.y = p1[q];
-            *reinterpret_cast<V2 *>(gb + q * qs) = w;
-        } else {
-            if (on0) gb[q * qs] = p0[q];
-            if (on1) gb[q * qs + 1] = p1[q];
-        }
-    }
-}
-
-template <typename real, int KD>
-__device__ __forceinline__ void direct_dir_x2_on(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool c0,
-                                                 bool c1, const real *p0, const real *p1)
-{
-    constexpr int ddx = ndir(KD, 0), ddy = ndir(KD, 1), ddz = ndir(KD, 2);
-    const int n0 = a.g.n[0], n1 = a.g.n[1], n2 = a.g.n[2];
-    const bool yz = (ddy == 0 || (ddy > 0 ? y == n1 - 1 : y == 0)) && (ddz == 0 || (ddz > 0 ? z == n2 - 1 : z == 0));
-    bool on0 = c0 && yz, on1 = c1 && yz;
-    if (ddx < 0) {
-        on0 = on0 && x0 == 0;
-        on1 = false;  // x0 + 1 > 0
-    } else if (ddx > 0) {
-        on0 = on0 && x0 == n0 - 1;
-        on1 = on1 && x0 + 1 == n0 - 1;
-    }
-    if (on0 || on1) direct_dir_x2<real, KD>(a, direct_ptr(a, patch, KD), x0, y, z, on0, on1, p0, p1);
-}
-
-template <typename real, int... KD>
-__device__ __forceinline__ void direct_dirs_x2(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool c0,
-                                               bool c1, const real *p0, const real *p1,
-                                               std::integer_sequence<int, KD...>)
-{
-    (direct_dir_x2_on<real, KD>(a, patch, x0, y, z, c0, c1, p0, p1), ...);
-}
-
-// Direct ghost stores of a cell pair (x0, x0 + 1) -- the pack / copy / unpack of
-// P:331-337 folded into the sweep: a fluid cell on a patch face or edge stores
-// each PDF that travels into the neighbour at d (5 per face, 1 per edge) into
-// that neighbour's ghost cell at the same global position, in the grid the
-// neighbour pulls from next step.  c0 / c1: the cell is fluid and in the box.
-// Warps off the y / z faces (y, z are warp-uniform) only handle the x faces,
-// whose neighbour pointer (nb_x) the kernel loaded up front with the PDFs, so
-// no dependent load sits at the end of the thread.
-static_assert(ndir(8, 0) == -1 && ndir(8, 1) == 0 && ndir(8, 2) == 0, "plan order: kd 8 = -x");
-static_assert(ndir(9, 0) == 1 && ndir(9, 1) == 0 && ndir(9, 2) == 0, "plan order: kd 9 = +x");
-
-template <typename real>
-__device__ __forceinline__ void direct_stores_x2(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool c0,
-                                                 bool c1, const real *p0, const real *p1, real *nb_x)
-{
-    const Geom &g = a.g;
-    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
-    const bool yzf = y == 0 || y == n1 - 1 || z == 0 || z == n2 - 1;
-    if (!yzf) {
-        const bool hi0 = c0 && x0 == n0 - 1, hi1 = c1 && x0 + 1 == n0 - 1;
-        if (x0 == 0) {
-            direct_dir_x2<real, 8>(a, nb_x, x0, y, z, c0, false, p0, p1);
-            if (hi0 || hi1) direct_dir_x2<real, 9>(a, direct_ptr(a, patch, 9), x0, y, z, hi0, hi1, p0, p1);
-        } else {
-            direct_dir_x2<real, 9>(a, nb_x, x0, y, z, hi0, hi1, p0, p1);
-        }
-        return;
-    }
-    direct_dirs_x2<real>(a, patch, x0, y, z, c0, c1, p0, p1, std::make_integer_sequence<int, NDIR>{});
-}
 
 template <typename real, int MINB, int STCS, bool DIRECT>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)

@@ -5,6 +5,7 @@
 
 #include "collide.cuh"
 #include "kernels.cuh"
+#include "direct_stores.cuh"
 #include "sweep_common.cuh"
 
 namespace lbm {
@@ -119,7 +120,8 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(cons
 // sweep, as sweep.cu does for the two-grid layout:
 //   LOCAL: a fluid cell g on a patch face / edge stores out_q, for each q that
 //          travels into the neighbour, into the neighbour's ghost copy of g at
-//          slot opp(q) -- what the neighbour's next PULL gathers there;
+//          slot opp(q) -- what the neighbour's next PULL gathers there (the
+//          two-grid store pattern, direct_stores.cuh with OPPSLOT);
 //   PULL:  a fluid cell x whose scatter target x + e_q lies in a neighbour patch
 //          (and is fluid) stores out_q into that cell of the neighbour, slot q --
 //          what the neighbour's next LOCAL reads.  Only fluid writers store:
@@ -129,34 +131,6 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_aa_kernel(cons
 // (oz, oy, ox) + 1 in base 3 -> neighbour direction kd of the plan order, -1: none
 __constant__ int8_t c_kd27[27] = {-1, 0,  -1, 1,  2,  3,  -1, 4,  -1, 5,  6,  7,  8, -1,
                                   9,  10, 11, 12, -1, 13, -1, 14, 15, 16, -1, 17, -1};
-
-template <typename real>
-__device__ __forceinline__ real *aa_nbr(const SweepArgs<real> &a, int patch, int kd)
-{
-    return (real *)__ldg(reinterpret_cast<const unsigned long long *>(a.dnbr + ((int64_t)patch * NDIR + kd) * 2));
-}
-
-template <typename real>
-__device__ __forceinline__ void aa_local_direct(const SweepArgs<real> &a, int patch, int x, int y, int z,
-                                                const real *p)
-{
-    const Geom &g = a.g;
-    const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
-#pragma unroll
-    for (int kd = 0; kd < NDIR; ++kd) {
-        const int ddx = ndir(kd, 0), ddy = ndir(kd, 1), ddz = ndir(kd, 2);
-        const bool on = (ddx == 0 || (ddx > 0 ? x == n0 - 1 : x == 0)) &&
-                        (ddy == 0 || (ddy > 0 ? y == n1 - 1 : y == 0)) &&
-                        (ddz == 0 || (ddz > 0 ? z == n2 - 1 : z == 0));
-        if (!on) continue;
-        real *nb = aa_nbr(a, patch, kd);
-        if (!nb) continue;
-        real *gc = nb + cell_index(g, x - ddx * n0, y - ddy * n1, z - ddz * n2);
-#pragma unroll
-        for (int q = 1; q < Q; ++q)
-            if (outgoing(q, kd)) gc[OPP(q) * g.qs] = p[q];
-    }
-}
 
 template <typename real>
 __device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int patch, int x, int y, int z, uint8_t k,
@@ -173,29 +147,57 @@ __device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int pat
         if ((ox | oy | oz) == 0) continue;   // target inside the patch
         if (k == 1 && f[q] != 0) continue;   // wall target: the bounce-back stays at x
         const int kd = c_kd27[(oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)];
-        real *nb = aa_nbr(a, patch, kd);
+        real *nb = direct_ptr(a, patch, kd);
         if (!nb) continue;
         nb[q * g.qs + cell_index(g, dx - ox * n0, dy - oy * n1, dz - oz * n2)] = p[q];
     }
 }
 
-// A pair (x0, x0 + 1): only cells on a patch face do anything.
+// PULL, a cell on the x face S (-1 / +1) and on no y / z face: its scatter
+// targets x + e_q with e_qx = S are the x neighbour's cells
+// (x + S - S n0, y + e_qy, z + e_qz); y +- 1, z +- 1 stay inside the patch.
+template <typename real, int S>
+__device__ __forceinline__ void aa_pull_xface(const SweepArgs<real> &a, real *nb, int x, int y, int z, uint8_t k,
+                                              const uint8_t *f, const real *p)
+{
+    if (!nb) return;
+    const Geom &g = a.g;
+    real *row = nb + cell_index(g, x + S - S * g.n[0], y, z);
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (EXf(q) != S) continue;
+        if (k == 1 && f[q] != 0) continue;  // wall target: the bounce-back stays at x
+        row[q * g.qs + EYf(q) * (int64_t)g.px + EZf(q) * g.plane] = p[q];
+    }
+}
+
+// A pair (x0, x0 + 1): only cells on a patch face do anything.  nb_x: the x
+// neighbour of the pair's x-face cell (-x if x0 == 0, else +x), loaded up front.
+// LOCAL stores like the two-grid sweep (direct_stores.cuh), into slot opp(q).
 template <typename real, bool PULL>
 __device__ __forceinline__ void aa_direct_pair(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool has1,
                                                uint8_t k0, uint8_t k1, const uint8_t *f0, const uint8_t *f1,
-                                               const real *p0, const real *p1)
+                                               const real *p0, const real *p1, real *nb_x)
 {
-    const Geom &g = a.g;
-    const bool yzf = y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1;  // warp-uniform
-    const bool c0 = k0 != 2 && (yzf || x0 == 0 || x0 == g.n[0] - 1);
-    const bool c1 = has1 && k1 != 2 && (yzf || x0 + 1 == g.n[0] - 1);
-    if (c0) {
-        if (PULL) aa_pull_direct<real>(a, patch, x0, y, z, k0, f0, p0);
-        else aa_local_direct<real>(a, patch, x0, y, z, p0);
+    if (!PULL) {
+        direct_stores_x2<real, true>(a, patch, x0, y, z, k0 != 2, has1 && k1 != 2, p0, p1, nb_x);
+        return;
     }
-    if (c1) {
-        if (PULL) aa_pull_direct<real>(a, patch, x0 + 1, y, z, k1, f1, p1);
-        else aa_local_direct<real>(a, patch, x0 + 1, y, z, p1);
+    const Geom &g = a.g;
+    const int n0 = g.n[0];
+    const bool yzf = y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1;  // warp-uniform
+    if (yzf) {
+        if (k0 != 2) aa_pull_direct<real>(a, patch, x0, y, z, k0, f0, p0);
+        if (has1 && k1 != 2) aa_pull_direct<real>(a, patch, x0 + 1, y, z, k1, f1, p1);
+        return;
+    }
+    if (x0 == 0) {
+        if (k0 != 2) aa_pull_xface<real, -1>(a, nb_x, x0, y, z, k0, f0, p0);
+        if (n0 == 1 && k0 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0, y, z, k0, f0, p0);
+        if (n0 == 2 && has1 && k1 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0 + 1, y, z, k1, f1, p1);
+    } else {
+        if (x0 == n0 - 1 && k0 != 2) aa_pull_xface<real, 1>(a, nb_x, x0, y, z, k0, f0, p0);
+        if (has1 && x0 + 1 == n0 - 1 && k1 != 2) aa_pull_xface<real, 1>(a, nb_x, x0 + 1, y, z, k1, f1, p1);
     }
 }
 
@@ -230,6 +232,8 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     const int64_t fbase = (int64_t)bx.patch * g.fs + cell;
     const uint8_t k0 = a.kind[fbase];
     const uint8_t k1 = has1 ? a.kind[fbase + 1] : (uint8_t)2;
+    real *nb_x = nullptr;  // x-face neighbour for the direct ghost stores, loaded with the PDFs
+    if (DIRECT && (x0 == 0 || x0 + 1 >= g.n[0] - 1)) nb_x = direct_ptr(a, bx.patch, x0 == 0 ? 8 : 9);
     real *A = a.dst + pbase;  // in place
     real p0[Q], p1[Q];
 #pragma unroll
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
             }
         }
     }
-    if (DIRECT) aa_direct_pair<real, PULL>(a, bx.patch, x0, y, z, has1, k0, k1, f0, f1, p0, p1);
+    if (DIRECT) aa_direct_pair<real, PULL>(a, bx.patch, x0, y, z, has1, k0, k1, f0, f1, p0, p1, nb_x);
 }
 
 template <typename real>
