@@ -32,15 +32,38 @@ __global__ void __launch_bounds__(128, 3) stream_kernel(const T *__restrict__ sr
     if (x0 >= n || y >= n) return;
     const long long cell = pbase + ((long long)(z + 1) * (n + 2) + (y + 1)) * px + x0 + xo;
     T a[Q], b[Q];
+    using V2 = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const long long sh = SHIFT ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
-        a[i] = __ldg(src + cell + i * qs - sh);
-        b[i] = __ldg(src + cell + i * qs - sh + 1);
+        if (SHIFT == 4 && cEX[i] != 0) {
+            // aligned pair at x0 (row shifted in y / z only) + the neighbour lane's element
+            const T *row = src + cell + i * qs - (sh - cEX[i]);
+            const V2 v = __ldg(reinterpret_cast<const V2 *>(row));
+            const int lane = threadIdx.x;
+            if (cEX[i] > 0) {  // need (x0 - 1, x0): (lane - 1's .y, my .x)
+                T up = __shfl_up_sync(0xffffffffu, v.y, 1);
+                if (lane == 0) up = __ldg(row - 1);
+                a[i] = up;
+                b[i] = v.x;
+            } else {           // need (x0 + 1, x0 + 2): (my .y, lane + 1's .x)
+                T dn = __shfl_down_sync(0xffffffffu, v.x, 1);
+                if (lane == 31) dn = __ldg(row + 2);
+                a[i] = v.y;
+                b[i] = dn;
+            }
+        } else if (!SHIFT || cEX[i] == 0) {
+            const V2 v = __ldg(reinterpret_cast<const V2 *>(src + cell + i * qs - sh));
+            a[i] = v.x;
+            b[i] = v.y;
+        } else {
+            a[i] = __ldg(src + cell + i * qs - sh);
+            b[i] = __ldg(src + cell + i * qs - sh + 1);
+        }
     }
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
-        const long long sh = SHIFT >= 2 ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
+        const long long sh = (SHIFT == 2 || SHIFT == 3) ? (cEX[i] + cEY[i] * (long long)px + cEZ[i] * plane) : 0;
         if (SHIFT == 3 && cEX[i] != 0) {
             // pair (x0, x0 + 1) of the destination row: e_x = +1 -> (b of lane - 1, a);
             // e_x = -1 -> (b, a of lane + 1); edge lanes store their stray element alone
@@ -165,12 +188,14 @@ void run(int n, int P)
         case 0: stream_kernel<T, 0><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
         case 1: stream_kernel<T, 1><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
         case 2: stream_kernel<T, 2><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
-        default: stream_kernel<T, 3><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        case 3: stream_kernel<T, 3><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
+        default: stream_kernel<T, 4><<<grid, block>>>(s, d, n, px, plane, qs, xo); break;
         }
     };
-    const char *names[4] = {"aligned 19-in/19-out", "pull-shifted 19-in/19-out", "pull reads + push-shifted writes",
-                            "pull reads + push writes, shuffle-aligned"};
-    for (int shift = 0; shift < 4; ++shift) {
+    const char *names[5] = {"aligned 19-in/19-out", "pull-shifted 19-in/19-out", "pull reads + push-shifted writes",
+                            "pull reads + push writes, shuffle-aligned",
+                            "pull-shifted, 2-vector loads + shuffles for e_x != 0"};
+    for (int shift = 0; shift < 5; ++shift) {
         for (int w = 0; w < 5; ++w) launch(shift, a, b);
         const int reps = 50;
         cudaEventRecord(e0);
