@@ -95,7 +95,8 @@ struct lbm_ctx {
     int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
     int num_sms = 148;
     int tma_variant = 0;            // tile shape (sweep_tma.cu TmaShape); env LBM_TMA_SHAPE
-    alignas(64) CUtensorMap tm_pdf[2];
+    alignas(64) CUtensorMap tm_pdf[2];   // PDF grids, boxes for the directions with e_x = 0
+    alignas(64) CUtensorMap tm_pdfs[2];  // the same grids, one 64-B chunk wider (e_x != 0)
     alignas(64) CUtensorMap tm_kind;
     alignas(64) CUtensorMap tm_flags;
     cudaStream_t stream = nullptr, comm_stream = nullptr;

@@ -85,10 +85,12 @@ template <typename real>
 void tma_tile_shape(int variant, int *tx, int *ty);
 template <typename real>
 cudaError_t make_tma_maps(const void *grid, const uint8_t *kind, const uint8_t *flags, int nlocal, const Geom &g,
-                          int variant, CUtensorMap *pdf_map, CUtensorMap *kind_map, CUtensorMap *flag_map);
+                          int variant, CUtensorMap *pdf_map, CUtensorMap *pdfs_map, CUtensorMap *kind_map,
+                          CUtensorMap *flag_map);
 template <typename real>
-cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &kind_map, const CUtensorMap &flag_map,
-                             const SweepArgs<real> &a, int64_t total_tiles, int num_sms, int variant, cudaStream_t s);
+cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &pdfs_map, const CUtensorMap &kind_map,
+                             const CUtensorMap &flag_map, const SweepArgs<real> &a, int64_t total_tiles, int num_sms,
+                             int variant, cudaStream_t s);
 
 template <typename real>
 cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,

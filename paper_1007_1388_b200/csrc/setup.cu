@@ -743,9 +743,11 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         for (int i = 0; i < 2; ++i) {
             cudaError_t e = ctx->esize == 8
                                 ? make_tma_maps<double>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
-                                                        ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags)
+                                                        ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_pdfs[i],
+                                                        &ctx->tm_kind, &ctx->tm_flags)
                                 : make_tma_maps<float>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
-                                                       ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_kind, &ctx->tm_flags);
+                                                       ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_pdfs[i],
+                                                       &ctx->tm_kind, &ctx->tm_flags);
             if (e != cudaSuccess) {
                 ctx->err = "cuTensorMapEncodeTiled failed for the PDF / kind arrays";
                 return bail(LBM_ERR_CUDA);

@@ -50,12 +50,12 @@ lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
         else
             e = launch_sweep_aa<float>(sweep_args<float>(ctx, b), b.tiles, pull, ctx->aa_variant[0], s);
     } else if (ctx->use_tma) {
-        const CUtensorMap &pm = ctx->tm_pdf[ctx->cur];
+        const CUtensorMap &pm = ctx->tm_pdf[ctx->cur], &psm = ctx->tm_pdfs[ctx->cur];
         if (ctx->esize == 8)
-            e = launch_sweep_tma<double>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
+            e = launch_sweep_tma<double>(pm, psm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
                                          ctx->num_sms, ctx->tma_variant, s);
         else
-            e = launch_sweep_tma<float>(pm, ctx->tm_kind, ctx->tm_flags, sweep_args<float>(ctx, b), b.tiles,
+            e = launch_sweep_tma<float>(pm, psm, ctx->tm_kind, ctx->tm_flags, sweep_args<float>(ctx, b), b.tiles,
                                         ctx->num_sms, ctx->tma_variant, s);
     } else if (ctx->esize == 8)
         e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant[1], s);

@@ -15,10 +15,14 @@
 // stage, collide and store with coalesced STG.
 //
 // Measured on this B200 (tools/tma_probe.cu): a tiled TMA load whose innermost
-// start offset is not 16-B aligned raises cudaErrorIllegalInstruction, so every
-// PDF box starts at the aligned column x0 - A (A = 16 B / sizeof(real)) and is
-// TX + 2A wide (the consumer reads direction i at column tx + A - e_ix), and
-// every tile starts at a multiple of 16 cells in x.
+// start offset is not 16-B aligned raises cudaErrorIllegalInstruction, and the
+// bulk engine reads DRAM in 64-B chunks.  So the 9 directions with e_ix = 0 load
+// exactly the tile's aligned rows (box TX wide), and the 10 with e_ix = +-1 load
+// one 64-B chunk more (box TX + C wide, C = 64 B / sizeof(real)): from x0 - C
+// for e_ix = +1 (pull from x - 1), from x0 for e_ix = -1 (pull from x + 1).
+// That is exactly the chunks a SIMT warp touches; one box of TX + 2A with A =
+// 16 B for all 19 directions read +25 % (profiles/r01_ncu_sweep_tma*).  Every
+// tile starts at a multiple of 16 cells in x.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -89,20 +93,19 @@ template <typename real, int TX, int TY, int STAGES, int CPS>
 struct TmaCfg {
     static constexpr int TT = TX * TY;                       // cells per tile = consumer threads
     static constexpr int THREADS = TT + 32;                  // + producer warp
-    static constexpr int A = 16 / (int)sizeof(real);         // alignment halo (elements)
-    static constexpr int BW = TX + 2 * A;                    // PDF box width (elements)
-    static constexpr int BOX_ELEMS = BW * TY;
-    static constexpr int BOX_BYTES = align128(BOX_ELEMS * (int)sizeof(real));  // 128-B aligned slots
+    static constexpr int C = 64 / (int)sizeof(real);         // one 64-B chunk (elements)
+    static constexpr int BWS = TX + C;                       // box width of the e_x != 0 directions
+    static constexpr int BOX_BYTES = align128(BWS * TY * (int)sizeof(real));  // 128-B aligned slots
     static constexpr int BOX_STRIDE = BOX_BYTES / (int)sizeof(real);
     static constexpr int FW = TX + 32;                       // flag box width (bytes, 16-B halo each side)
     static constexpr int FPLANE = FW * (TY + 2);
     static constexpr int KIND_OFF = Q * BOX_BYTES;
     static constexpr int FLAG_OFF = KIND_OFF + align128(TT);
     static constexpr int STAGE_STRIDE = FLAG_OFF + align128(3 * FPLANE);
-    static constexpr int TX_BYTES = Q * BOX_ELEMS * (int)sizeof(real) + TT + 3 * FPLANE;  // delivered per stage
+    static constexpr int TX_BYTES = (9 * TX + 10 * BWS) * TY * (int)sizeof(real) + TT + 3 * FPLANE;  // per stage
     static constexpr int BAR_OFF = STAGES * STAGE_STRIDE;
     static constexpr int SMEM = BAR_OFF + STAGES * (16 + 32);
-    static_assert(TX % 16 == 0, "tile x must keep 16-B aligned TMA starts");
+    static_assert(TX % 16 == 0 && TX % C == 0, "tile x must keep 64-B aligned TMA starts");
     static_assert(SMEM <= 232448 / CPS - 1024, "shared memory budget");
 };
 
@@ -114,8 +117,9 @@ struct TileMeta {
 
 template <typename real, int TX, int TY, int STAGES, int CPS>
 __global__ void __launch_bounds__(TmaCfg<real, TX, TY, STAGES, CPS>::THREADS, CPS)
-    sweep_tma_kernel(const __grid_constant__ CUtensorMap tm_pdf, const __grid_constant__ CUtensorMap tm_kind,
-                     const __grid_constant__ CUtensorMap tm_flags, const SweepArgs<real> a, const int64_t total_tiles)
+    sweep_tma_kernel(const __grid_constant__ CUtensorMap tm_pdf, const __grid_constant__ CUtensorMap tm_pdfs,
+                     const __grid_constant__ CUtensorMap tm_kind, const __grid_constant__ CUtensorMap tm_flags,
+                     const SweepArgs<real> a, const int64_t total_tiles)
 {
     using C = TmaCfg<real, TX, TY, STAGES, CPS>;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -139,6 +143,7 @@ __global__ void __launch_bounds__(TmaCfg<real, TX, TY, STAGES, CPS>::THREADS, CP
         // ---------------- producer warp (one lane issues all TMA traffic)
         if (tid == 0) {
             prefetch_tmap(&tm_pdf);
+            prefetch_tmap(&tm_pdfs);
             prefetch_tmap(&tm_kind);
             prefetch_tmap(&tm_flags);
             int stage = 0;
@@ -172,13 +177,17 @@ __global__ void __launch_bounds__(TmaCfg<real, TX, TY, STAGES, CPS>::THREADS, CP
                 meta[stage] = m;
                 unsigned char *sb = smem + stage * C::STAGE_STRIDE;
                 mbar_arrive_expect_tx(&full[stage], (uint32_t)C::TX_BYTES);
-                // Pull boxes: direction i at (x0 - A, y0 - ey, z - ez) of q-slice i
-                // (padded coordinates: interior x = 0 is column xo, y = 0 row 1, z = 0 plane 1).
+                // Pull boxes of q-slice i, rows y0 - ey, plane z - ez (padded coordinates:
+                // interior x = 0 is column xo, y = 0 row 1, z = 0 plane 1).
                 const int cx = m.x0 + g.xo, cy = m.y0 + 1, cz = m.z + 1, cq = m.patch * Q;
 #pragma unroll
-                for (int i = 0; i < Q; ++i)
-                    tma_load_4d(sb + i * C::BOX_BYTES, &tm_pdf, cx - C::A, cy - EY(i), cz - EZ(i), cq + i,
-                                &full[stage]);
+                for (int i = 0; i < Q; ++i) {
+                    if (EX(i) == 0)
+                        tma_load_4d(sb + i * C::BOX_BYTES, &tm_pdf, cx, cy - EY(i), cz - EZ(i), cq + i, &full[stage]);
+                    else
+                        tma_load_4d(sb + i * C::BOX_BYTES, &tm_pdfs, EX(i) > 0 ? cx - C::C : cx, cy - EY(i),
+                                    cz - EZ(i), cq + i, &full[stage]);
+                }
                 tma_load_4d(sb + C::KIND_OFF, &tm_kind, cx, cy, cz, m.patch, &full[stage]);
                 tma_load_4d(sb + C::FLAG_OFF, &tm_flags, cx - 16, cy - 1, cz - 1, m.patch, &full[stage]);
                 if (++stage == STAGES) {
@@ -205,7 +214,9 @@ __global__ void __launch_bounds__(TmaCfg<real, TX, TY, STAGES, CPS>::THREADS, CP
         const real *box = reinterpret_cast<const real *>(smem + sbase);
         real p[Q];
 #pragma unroll
-        for (int i = 0; i < Q; ++i) p[i] = box[i * C::BOX_STRIDE + cyl * C::BW + cxl + C::A - EX(i)];
+        for (int i = 0; i < Q; ++i)
+            p[i] = EX(i) == 0 ? box[i * C::BOX_STRIDE + cyl * TX + cxl]
+                              : box[i * C::BOX_STRIDE + cyl * C::BWS + cxl + (EX(i) > 0 ? C::C - 1 : 1)];
         const uint8_t k = smem[sbase + C::KIND_OFF + c];
         uint8_t nbf[Q];
         if (k == 1) {
@@ -307,17 +318,21 @@ static cudaError_t encode4(CUtensorMap *map, CUtensorMapDataType dt, int esize, 
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// Maps: PDFs [19 * nlocal][nz + 2][py][px] (box (TX + 2A) x TY), kinds and
-// flags [nlocal][nz + 2][py][px] bytes (boxes TX x TY and (TX + 32) x (TY + 2) x 3).
+// Maps: PDFs [19 * nlocal][nz + 2][py][px] (boxes TX x TY and (TX + C) x TY,
+// C = 64 B / sizeof(real)), kinds and flags [nlocal][nz + 2][py][px] bytes
+// (boxes TX x TY and (TX + 32) x (TY + 2) x 3).
 template <typename real>
 cudaError_t make_tma_maps(const void *grid, const uint8_t *kind, const uint8_t *flags, int nlocal, const Geom &g,
-                          int variant, CUtensorMap *pdf_map, CUtensorMap *kind_map, CUtensorMap *flag_map)
+                          int variant, CUtensorMap *pdf_map, CUtensorMap *pdfs_map, CUtensorMap *kind_map,
+                          CUtensorMap *flag_map)
 {
     int TX, TY;
     tma_tile_shape<real>(variant, &TX, &TY);
-    const int A = 16 / (int)sizeof(real);
-    cudaError_t e = encode4(pdf_map, sizeof(real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                            (int)sizeof(real), grid, g, (cuuint64_t)Q * nlocal, TX + 2 * A, TY, 1);
+    const int Cw = 64 / (int)sizeof(real);
+    const CUtensorMapDataType dt = sizeof(real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    cudaError_t e = encode4(pdf_map, dt, (int)sizeof(real), grid, g, (cuuint64_t)Q * nlocal, TX, TY, 1);
+    if (e != cudaSuccess) return e;
+    e = encode4(pdfs_map, dt, (int)sizeof(real), grid, g, (cuuint64_t)Q * nlocal, TX + Cw, TY, 1);
     if (e != cudaSuccess) return e;
     if (kind_map) {
         e = encode4(kind_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, kind, g, nlocal, TX, TY, 1);
@@ -328,8 +343,9 @@ cudaError_t make_tma_maps(const void *grid, const uint8_t *kind, const uint8_t *
 }
 
 template <typename real, int V>
-static cudaError_t launch_v(const CUtensorMap &pm, const CUtensorMap &km, const CUtensorMap &fm,
-                            const SweepArgs<real> &a, int64_t total_tiles, int num_sms, cudaStream_t s)
+static cudaError_t launch_v(const CUtensorMap &pm, const CUtensorMap &psm, const CUtensorMap &km,
+                            const CUtensorMap &fm, const SweepArgs<real> &a, int64_t total_tiles, int num_sms,
+                            cudaStream_t s)
 {
     constexpr int TX = TmaShape<real, V>::TX, TY = TmaShape<real, V>::TY, ST = TmaShape<real, V>::ST;
     constexpr int CPS = TmaShape<real, V>::CPS;
@@ -340,31 +356,35 @@ static cudaError_t launch_v(const CUtensorMap &pm, const CUtensorMap &km, const 
     if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * CPS;
     if (grid > total_tiles) grid = total_tiles;
-    sweep_tma_kernel<real, TX, TY, ST, CPS><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(pm, km, fm, a, total_tiles);
+    sweep_tma_kernel<real, TX, TY, ST, CPS><<<(unsigned)grid, C::THREADS, C::SMEM, s>>>(pm, psm, km, fm, a,
+                                                                                       total_tiles);
     return cudaGetLastError();
 }
 
 template <typename real>
-cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &kind_map, const CUtensorMap &flag_map,
-                             const SweepArgs<real> &a, int64_t total_tiles, int num_sms, int variant, cudaStream_t s)
+cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &pdfs_map, const CUtensorMap &kind_map,
+                             const CUtensorMap &flag_map, const SweepArgs<real> &a, int64_t total_tiles, int num_sms,
+                             int variant, cudaStream_t s)
 {
     if (total_tiles <= 0) return cudaSuccess;
     switch (variant) {
-    case 1: return launch_v<real, 1>(pdf_map, kind_map, flag_map, a, total_tiles, num_sms, s);
-    case 2: return launch_v<real, 2>(pdf_map, kind_map, flag_map, a, total_tiles, num_sms, s);
-    default: return launch_v<real, 0>(pdf_map, kind_map, flag_map, a, total_tiles, num_sms, s);
+    case 1: return launch_v<real, 1>(pdf_map, pdfs_map, kind_map, flag_map, a, total_tiles, num_sms, s);
+    case 2: return launch_v<real, 2>(pdf_map, pdfs_map, kind_map, flag_map, a, total_tiles, num_sms, s);
+    default: return launch_v<real, 0>(pdf_map, pdfs_map, kind_map, flag_map, a, total_tiles, num_sms, s);
     }
 }
 
 template void tma_tile_shape<float>(int, int *, int *);
 template void tma_tile_shape<double>(int, int *, int *);
 template cudaError_t make_tma_maps<float>(const void *, const uint8_t *, const uint8_t *, int, const Geom &, int,
-                                          CUtensorMap *, CUtensorMap *, CUtensorMap *);
+                                          CUtensorMap *, CUtensorMap *, CUtensorMap *, CUtensorMap *);
 template cudaError_t make_tma_maps<double>(const void *, const uint8_t *, const uint8_t *, int, const Geom &, int,
-                                           CUtensorMap *, CUtensorMap *, CUtensorMap *);
+                                           CUtensorMap *, CUtensorMap *, CUtensorMap *, CUtensorMap *);
 template cudaError_t launch_sweep_tma<float>(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
-                                             const SweepArgs<float> &, int64_t, int, int, cudaStream_t);
+                                             const CUtensorMap &, const SweepArgs<float> &, int64_t, int, int,
+                                             cudaStream_t);
 template cudaError_t launch_sweep_tma<double>(const CUtensorMap &, const CUtensorMap &, const CUtensorMap &,
-                                              const SweepArgs<double> &, int64_t, int, int, cudaStream_t);
+                                              const CUtensorMap &, const SweepArgs<double> &, int64_t, int, int,
+                                              cudaStream_t);
 
 }  // namespace lbm
