@@ -77,7 +77,7 @@ cudaError_t launch_signal_peers(unsigned long long *epoch, unsigned long long *c
                                 cudaStream_t s);
 // variants 12..15: two cells per thread along x, 2-vector accesses,
 // min blocks 4 / 5 of 128 threads, stcs 0 / 1.
-constexpr int kSweepVariants = 18;  // 16 / 17: persistent x2 (sweep.cu)
+constexpr int kSweepVariants = 16;
 __host__ __device__ constexpr int sweep_cells_z(int variant) { return (variant >= 8 && variant < 12) ? 2 : 1; }
 
 // TMA-staged persistent sweep (sweep_tma.cu); variant selects the tile shape.

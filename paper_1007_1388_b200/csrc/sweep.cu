@@ -11,7 +11,6 @@
 // independent loads in flight per SM and fully coalesced, sector-aligned
 // stores.  Default: sweep_x2_kernel (two cells per thread), optionally storing
 // the outgoing PDFs of patch-face cells straight into neighbour ghost layers.
-#include <algorithm>
 #include <cstdint>
 #include <utility>
 
@@ -114,11 +113,11 @@ __global__ void __launch_bounds__(SWEEP_BX *SWEEP_BY, MINB) sweep_kernel(const S
 // neighbours and must not be overwritten.  Block (32, 4) threads = 64 x 4 cells.
 
 
-// One 64 x 4 tile (block b of the tile list) of the two-cells-per-thread sweep.
-template <typename real, int STCS, bool DIRECT>
-__device__ __forceinline__ void sweep_x2_tile(const SweepArgs<real> &a, const int64_t b)
+template <typename real, int MINB, int STCS, bool DIRECT>
+__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)
 {
     using V2 = typename Vec2<real>::T;
+    const int64_t b = blockIdx.x;
     int lo = 0, hi = a.nboxes;
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -226,50 +225,12 @@ __device__ __forceinline__ void sweep_x2_tile(const SweepArgs<real> &a, const in
     if (DIRECT) direct_stores_x2<real>(a, bx.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);
 }
 
-template <typename real, int MINB, int STCS, bool DIRECT>
-__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)
-{
-    sweep_x2_tile<real, STCS, DIRECT>(a, blockIdx.x);
-}
-
-// Persistent form: one wave of blocks walks the tile list (variants 16 / 17).
-template <typename real, int MINB, bool DIRECT>
-__global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_persist_kernel(const SweepArgs<real> a,
-                                                                                const int64_t total_tiles)
-{
-    for (int64_t b = blockIdx.x; b < total_tiles; b += gridDim.x) sweep_x2_tile<real, 0, DIRECT>(a, b);
-}
-
-static int sm_count()
-{
-    static int dev = -1, sms = 148;
-    int d = 0;
-    if (cudaGetDevice(&d) == cudaSuccess && d != dev) {
-        int v = 0;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) == cudaSuccess && v > 0) sms = v;
-        dev = d;
-    }
-    return sms;
-}
-
 template <typename real>
 static bool launch_x2(const SweepArgs<real> &a, unsigned grid, int variant, cudaStream_t s)
 {
     dim3 block(32, SWEEP_BY, 1);
     // min blocks of 128 threads: fp32 4 / 5, fp64 2 / 3 (38 live doubles per thread)
     constexpr int M0 = sizeof(real) == 8 ? 2 : 4, M1 = sizeof(real) == 8 ? 3 : 5;
-    if (variant >= 16) {  // persistent: one wave of min-blocks x SMs blocks
-        const int m = variant == 16 ? M0 : M1;
-        const unsigned pg = (unsigned)std::min<int64_t>(grid, (int64_t)sm_count() * m);
-        if (a.dnbr) {
-            if (variant == 16) sweep_x2_persist_kernel<real, M0, true><<<pg, block, 0, s>>>(a, grid);
-            else sweep_x2_persist_kernel<real, M1, true><<<pg, block, 0, s>>>(a, grid);
-        } else {
-            if (variant == 16) sweep_x2_persist_kernel<real, M0, false><<<pg, block, 0, s>>>(a, grid);
-            else sweep_x2_persist_kernel<real, M1, false><<<pg, block, 0, s>>>(a, grid);
-        }
-        return true;
-    }
     if (a.dnbr) {
         switch (variant) {
         case 12: sweep_x2_kernel<real, M0, 0, true><<<grid, block, 0, s>>>(a); break;
