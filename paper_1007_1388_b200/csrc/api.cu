@@ -138,7 +138,7 @@ LBM_API lbm_status lbm_synchronize(lbm_ctx *ctx)
     if (ctx->d_error && ctx->npeers_direct > 0) {
         int err = 0;
         CK(cudaMemcpy(&err, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
-        if (err) return ctx->fail(LBM_ERR_INTERNAL, "fused exchange: a peer GPU did not reach the step barrier");
+        if (err) return ctx->fail(LBM_ERR_INTERNAL, "fused exchange: a peer GPU did not reach the step barrier within LBM_PEER_TIMEOUT_S (default 120 s)");
     }
     if (ctx->timing) return flush_timing(ctx);
     return LBM_OK;

@@ -18,12 +18,14 @@
 // with wait_peers_kernel, which acquires until every peer's epoch has caught
 // up -- i.e. the peers have finished reading the grid this rank is about to
 // overwrite and have finished writing the ghosts it is about to read.  Bounded
-// spin: after ~20 s it reports an error instead of hanging.  Only the shell
+// wait (120 s by default, LBM_PEER_TIMEOUT_S): it reports an error instead of
+// hanging.  Only the shell
 // sweeps touch ghost layers (read or remote write), so only they are ordered
 // by the handshake; the interior sweep never waits for a peer.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "collide.cuh"
 #include "kernels.cuh"
@@ -153,17 +155,29 @@ __global__ void signal_peers_kernel(unsigned long long *epoch, unsigned long lon
 }
 
 // Wait until every peer has finished the step this rank just finished.
+__device__ __forceinline__ unsigned long long globaltimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Bounded by wall time (timeout_ns, env LBM_PEER_TIMEOUT_S, default 120 s): a
+// peer that never arrives (its process died) is reported through *error and
+// lbm_synchronize instead of hanging the GPU; a peer that is merely late (host
+// work between its steps) is waited for.
 __global__ void wait_peers_kernel(const unsigned long long *inbox, const int *peer_rank, int npeers,
-                                  const unsigned long long *epoch, int *error)
+                                  const unsigned long long *epoch, int *error, unsigned long long timeout_ns)
 {
     const int i = threadIdx.x;
     if (i >= npeers) return;
     const unsigned long long target = *epoch;
     const unsigned long long *slot = inbox + peer_rank[i];
-    unsigned long long spins = 0;
+    if (ld_acquire_sys(slot) >= target) return;
+    const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(slot) < target) {
-        __nanosleep(64);
-        if (++spins > (1ull << 28)) {  // ~20 s: a peer is gone -- report, never hang
+        __nanosleep(256);
+        if (globaltimer_ns() - t0 > timeout_ns) {
             atomicExch(error, 1);
             return;
         }
@@ -198,7 +212,13 @@ cudaError_t launch_wait_peers(const unsigned long long *inbox, const int *peer_r
                               const unsigned long long *epoch, int *error, cudaStream_t s)
 {
     if (npeers <= 0) return cudaSuccess;
-    wait_peers_kernel<<<1, 32, 0, s>>>(inbox, peer_rank, npeers, epoch, error);
+    static unsigned long long timeout_ns = 0;
+    if (!timeout_ns) {
+        const char *e = std::getenv("LBM_PEER_TIMEOUT_S");
+        const double sec = e ? std::atof(e) : 120.0;
+        timeout_ns = (unsigned long long)((sec > 0 ? sec : 120.0) * 1e9);
+    }
+    wait_peers_kernel<<<1, 32, 0, s>>>(inbox, peer_rank, npeers, epoch, error, timeout_ns);
     return cudaGetLastError();
 }
 

@@ -62,3 +62,11 @@ def test_full_size_bitwise_vs_one_gpu(n, config):
     if _gpus() < n:
         pytest.skip(f"needs {n} GPUs")
     assert _torchrun(n, "mgpu_fullsize_worker.py", config, timeout=900).returncode == 0
+
+
+def test_peer_timeout_reports_error():
+    """A peer that stops stepping makes the fused exchange report an error
+    (LBM_ERR_INTERNAL from lbm_step after LBM_PEER_TIMEOUT_S) -- never a hang."""
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    assert _torchrun(2, "mgpu_timeout_worker.py", timeout=300).returncode == 0
