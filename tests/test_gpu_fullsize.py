@@ -21,12 +21,16 @@ def plane_cells(nx, ny, z0, z1):
     return np.stack([xx.ravel(), yy.ravel(), zz.ravel()], 1)
 
 
-@pytest.mark.parametrize("n,prec,patch", [(256, 8, 256), (256, 4, 256), (384, 8, 384), (256, 4, 64)])
-def test_full_size_sampled_planes(n, prec, patch):
+@pytest.mark.parametrize("n,prec,patch,layout", [(256, 8, 256, "ab"), (256, 4, 256, "ab"), (384, 8, 384, "ab"),
+                                                 (256, 4, 64, "ab"), (256, 8, 256, "aa"), (256, 4, 64, "aa")])
+def test_full_size_sampled_planes(n, prec, patch, layout):
+    """AA cases: the 5 warm-up steps leave the streamed state (odd count), the
+    sampled step the swapped one -- both representations are read back."""
     from paper_1007_1388_b200 import lbm
     N = (n, n, n)
     fl, wu = inputs.ldc_flags(N)
-    L = lbm.Lattice(N, (patch,) * 3, inputs.LDC_OMEGA, prec, device=0)
+    L = lbm.Lattice(N, (patch,) * 3, inputs.LDC_OMEGA, prec, device=0,
+                    layout=lbm.LBM_LAYOUT_AA if layout == "aa" else lbm.LBM_LAYOUT_AB)
     try:
         L.set_flags(fl, wu)
         L.init_noise(inputs.NOISE_SEED)
