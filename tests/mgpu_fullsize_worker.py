@@ -4,12 +4,14 @@
 SURVEY 8(d) row 3: "1 vs N GPUs bitwise at full size for 10 steps".  The
 BASELINE weak-scaling configuration -- 384^3 fp64 per GPU, process grid
 1x1x2 / 1x2x2 / 2x2x2, lid-driven cavity, dyadic noise start -- runs 10 steps
-decomposed over the ranks with the default exchange (fused NVLink stores).
+decomposed over the ranks with the default exchange (fused NVLink stores);
+also "strong" (768^3 in 384^3 patches), "patchy" (384^3 fp32 per GPU in 64^3
+patches) and "aa" (256^3 fp64 per GPU, AA layout).
 Every rank samples the PDFs of its brick at: every cell of the planes on both
 sides of each process cut (which contain the edge lines where three bricks
 meet), and seeded random cells.  Rank 0 then runs the whole domain on one GPU
-(config "strong": 768^3 in 8 patches of 384^3, the strong-scaling config) and
-compares the samples bitwise.  Exit code 0 = pass.
+(same patches, precision and layout) and compares the samples bitwise.  Exit
+code 0 = pass.
 """
 import os
 import sys
@@ -64,16 +66,21 @@ def main():
     dist.init_process_group("gloo")
     from paper_1007_1388_b200 import inputs, lbm
     pgrid = GRIDS[world]
+    prec, layout = lbm.LBM_FP64, lbm.LBM_LAYOUT_AB
     if config == "weak":
         domain, patch = tuple(N * p for p in pgrid), (N, N, N)
-    else:  # strong: 768^3 in 8 patches of 384^3, 8 / world patches per GPU
+    elif config == "strong":  # 768^3 in 8 patches of 384^3, 8 / world patches per GPU
         domain, patch = (2 * N, 2 * N, 2 * N), (N, N, N)
+    elif config == "patchy":  # 384^3 fp32 per GPU in 216 patches of 64^3 (BASELINE config 5)
+        domain, patch, prec = tuple(N * p for p in pgrid), (64, 64, 64), lbm.LBM_FP32
+    else:  # aa: 256^3 fp64 per GPU, AA layout
+        domain, patch, layout = tuple(256 * p for p in pgrid), (256, 256, 256), lbm.LBM_LAYOUT_AA
     fl, wu = inputs.ldc_flags(domain)
     cells = samples(domain, pgrid, np.random.default_rng(1007))
     obj = [lbm.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, lbm.LBM_FP64, device=local, rank=rank, nranks=world,
-                    nccl_id=obj[0], proc_grid=pgrid)
+    L = lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, rank=rank, nranks=world,
+                    nccl_id=obj[0], proc_grid=pgrid, layout=layout)
     L.set_flags(fl, wu)
     L.init_noise(inputs.NOISE_SEED)
     L.step(STEPS)
@@ -89,7 +96,7 @@ def main():
         got_cells = np.concatenate([p[0] for p in parts])
         got = np.concatenate([p[1] for p in parts])
         assert got_cells.shape[0] == cells.shape[0], "every sample is owned by exactly one rank"
-        with lbm.Lattice(domain, patch, inputs.LDC_OMEGA, lbm.LBM_FP64, device=local) as L1:
+        with lbm.Lattice(domain, patch, inputs.LDC_OMEGA, prec, device=local, layout=layout) as L1:
             L1.set_flags(fl, wu)
             L1.init_noise(inputs.NOISE_SEED)
             L1.step(STEPS)

@@ -54,7 +54,8 @@ def test_nccl_exchange_matches_single_gpu(n):
     assert _torchrun(n, "mgpu_worker.py").returncode == 0
 
 
-@pytest.mark.parametrize("n,config", [(2, "weak"), (4, "weak"), (2, "strong")])
+@pytest.mark.parametrize("n,config", [(2, "weak"), (4, "weak"), (2, "strong"), (2, "patchy"), (2, "aa"),
+                                      (4, "patchy")])
 def test_full_size_bitwise_vs_one_gpu(n, config):
     """BASELINE weak-scaling config (384^3 fp64 per GPU) and strong-scaling config
     (768^3 in 8 patches of 384^3) at full size, 10 steps: N-GPU samples across
