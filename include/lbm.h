@@ -234,6 +234,14 @@ LBM_API lbm_status lbm_get_pdfs_at(lbm_ctx *ctx, const int64_t *xyz, int64_t n, 
  * rho_out: double [z][y][x]; u_out: double [z][y][x][3].  Either may be NULL. */
 LBM_API lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho_out, double *u_out);
 
+/* Total mass of the whole lattice: sum over all fluid cells of rho = rho0 +
+ * sum_i f~_i (conserved by the collision and the bounce-back,
+ * SURVEY V6), computed on the device in fp64 (deterministic on each rank) and
+ * summed over the ranks with one NCCL all-reduce -- a collective: every rank
+ * must call it.  Off the hot path (reads the whole state).  mass_out: caller-
+ * owned double, the same value on every rank.                                */
+LBM_API lbm_status lbm_total_mass(lbm_ctx *ctx, double *mass_out);
+
 LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out);
 
 /* Enable (1) / disable (0) per-phase CUDA-event timing inside lbm_step;

@@ -212,6 +212,32 @@ LBM_API lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho_out, double *u_
     return transfer_chunks(ctx, nullptr, false, 1, rho_out, u_out);
 }
 
+LBM_API lbm_status lbm_total_mass(lbm_ctx *ctx, double *mass_out)
+{
+    CHECK_CTX(ctx);
+    if (!mass_out) return ctx->fail(LBM_ERR_ARG, "mass_out is NULL");
+    lbm_status st;
+    if (!ctx->d_mass && (st = dev_alloc(ctx, &ctx->d_mass, (size_t)(kMassBlocks + 1) * sizeof(double)))) return st;
+    const Decomp &d = ctx->dec;
+    const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
+    // representation of the state in the grid (aux_kernels.cu rep_slot / read_state)
+    const int rep = ctx->layout == LBM_LAYOUT_AA ? (ctx->aa_phase == 0 ? 1 : 2) : 0;
+    double *sum = ctx->d_mass + kMassBlocks;
+    const cudaError_t e =
+        ctx->esize == 8 ? launch_mass<double>((const double *)ctx->grid[ctx->cur], ctx->flags, d.owned_lo, on, d.brick,
+                                              ctx->g, rep, (const double *)ctx->corr, ctx->d_mass, sum, ctx->stream)
+                        : launch_mass<float>((const float *)ctx->grid[ctx->cur], ctx->flags, d.owned_lo, on, d.brick,
+                                             ctx->g, rep, (const float *)ctx->corr, ctx->d_mass, sum, ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "mass_kernel", __FILE__, __LINE__);
+    ctx->launches += 2;
+    if (ctx->nccl) NK(ncclAllReduce(sum, sum, 1, ncclFloat64, ncclSum, ctx->nccl, ctx->stream));
+    double dsum = 0.0;
+    CK(cudaMemcpyAsync(&dsum, sum, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *mass_out = (double)ctx->fluid_global + dsum;  // rho0 = 1 per fluid cell + sum of delta rho
+    return LBM_OK;
+}
+
 static void fill_info_decomp(const Decomp &d, int esize, const SegLists &segs, lbm_info *out)
 {
     for (int a = 0; a < 3; ++a) {

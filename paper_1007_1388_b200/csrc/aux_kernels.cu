@@ -277,6 +277,73 @@ cudaError_t launch_export(const real *grid, const uint8_t *flags, int64_t z0, in
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- total mass
+// sum of delta rho = sum_i f~_i over the owned fluid cells in fp64,
+// deterministic: a fixed grid of kMassBlocks blocks, each thread summing its cells
+// in order, a tree per block into partial[b], then one block summing the
+// partials in order (lbm_total_mass; off the hot path).
+template <typename real>
+__global__ void __launch_bounds__(kMassThreads) mass_kernel(const real *grid, const uint8_t *flags, int64_t ncells,
+                                                            int64_t nx, int64_t ny, int b0, int b1, int b2,
+                                                            const Geom g, const int rep, const real *corr,
+                                                            double *partial)
+{
+    const int brick[3] = {b0, b1, b2};
+    double s = 0.0;
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t ox = c % nx;
+        const int64_t r = c / nx;
+        const int64_t oy = r % ny;
+        const int64_t oz = r / ny;
+        int lp, lx, ly, lz;
+        owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
+        const int64_t ci = cell_index(g, lx, ly, lz);
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        if (fp[0] != 0) continue;
+        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        double cs = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) cs += read_state(gp, fp, corr, g, rep, q);
+        s += cs;
+    }
+    __shared__ double sh[kMassThreads];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kMassThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(kMassThreads) mass_finish_kernel(const double *partial, double *out)
+{
+    __shared__ double sh[kMassThreads];
+    double s = 0.0;
+    for (int b = threadIdx.x; b < kMassBlocks; b += kMassThreads) s += partial[b];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = kMassThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+template <typename real>
+cudaError_t launch_mass(const real *grid, const uint8_t *flags, const int64_t owned_lo[3], const int64_t on[3],
+                        const int brick[3], const Geom &g, int rep, const real *corr, double *partial, double *out,
+                        cudaStream_t s)
+{
+    (void)owned_lo;
+    const int64_t ncells = on[0] * on[1] * on[2];
+    mass_kernel<real><<<kMassBlocks, kMassThreads, 0, s>>>(grid, flags, ncells, on[0], on[1], brick[0], brick[1],
+                                                          brick[2], g, rep, corr, partial);
+    mass_finish_kernel<<<1, kMassThreads, 0, s>>>(partial, out);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- seeded noise (input generator)
 // Same counter-based generator as paper_1007_1388_b200/inputs.py (not part of
 // the method): k = splitmix64(global_index * 19 + q + seed * golden) % 2049 - 1024.
@@ -411,6 +478,9 @@ cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind
                                              double *, double *, int, const real *, cudaStream_t);             \
     template cudaError_t launch_noise<real>(real *, uint64_t, const int64_t *, const int64_t *, const int64_t *, \
                                             const int *, const Geom &, int, cudaStream_t);                     \
+    template cudaError_t launch_mass<real>(const real *, const uint8_t *, const int64_t *, const int64_t *,       \
+                                           const int *, const Geom &, int, const real *, double *, double *,   \
+                                           cudaStream_t);                                                      \
     template cudaError_t launch_gather<real>(const real *, const uint8_t *, const int64_t *, int64_t,            \
                                              const int *, const Geom &, double *, int, const real *,           \
                                              cudaStream_t);

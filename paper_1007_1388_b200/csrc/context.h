@@ -146,6 +146,7 @@ struct lbm_ctx {
     int64_t steps = 0, launches = 0;
     int64_t launches_per_step = 0;
     int64_t device_bytes = 0;
+    double *d_mass = nullptr;  // lbm_total_mass scratch: kMassBlocks partials + the sum
     std::string err;
     bool poisoned = false;
     bool timing = false;

@@ -92,6 +92,14 @@ cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &pdfs
                              const CUtensorMap &flag_map, const SweepArgs<real> &a, int64_t total_tiles, int num_sms,
                              int variant, cudaStream_t s);
 
+// Total mass: sum of delta rho over the owned fluid cells into *out (fp64,
+// deterministic; partial: kMassBlocks doubles of scratch).
+constexpr int kMassBlocks = 1024, kMassThreads = 256;
+template <typename real>
+cudaError_t launch_mass(const real *grid, const uint8_t *flags, const int64_t owned_lo[3], const int64_t on[3],
+                        const int brick[3], const Geom &g, int rep, const real *corr, double *partial, double *out,
+                        cudaStream_t s);
+
 template <typename real>
 cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elems, const real *grid_src,
                                  real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,

@@ -450,7 +450,7 @@ void destroy_ctx(lbm_ctx *ctx)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->d_lnbr, (void *)ctx->d_dnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
+    for (void *p : {(void *)ctx->d_mass, (void *)ctx->d_lnbr, (void *)ctx->d_dnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
                     (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
         if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)

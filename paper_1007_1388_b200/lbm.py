@@ -29,7 +29,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblbm_b200
 EXPORTED = ("lbm_abi_version", "lbm_config_default", "lbm_create", "lbm_create_ex", "lbm_destroy",
             "lbm_set_flags", "lbm_get_flags", "lbm_set_pdfs", "lbm_init_noise", "lbm_step",
             "lbm_step_async", "lbm_synchronize", "lbm_get_pdfs", "lbm_get_pdfs_at",
-            "lbm_get_macroscopic", "lbm_get_info", "lbm_set_timing", "lbm_get_stream",
+            "lbm_get_macroscopic", "lbm_total_mass", "lbm_get_info", "lbm_set_timing", "lbm_get_stream",
             "lbm_last_error", "lbm_nccl_unique_id", "lbm_plan")
 
 
@@ -95,6 +95,7 @@ def _load() -> ctypes.CDLL:
         "lbm_get_pdfs": (c.c_int, [c.c_void_p, c.c_void_p]),
         "lbm_get_pdfs_at": (c.c_int, [c.c_void_p, c.c_void_p, c.c_int64, c.c_void_p]),
         "lbm_get_macroscopic": (c.c_int, [c.c_void_p, c.c_void_p, c.c_void_p]),
+        "lbm_total_mass": (c.c_int, [c.c_void_p, P(c.c_double)]),
         "lbm_get_info": (c.c_int, [c.c_void_p, P(LbmInfo)]),
         "lbm_set_timing": (c.c_int, [c.c_void_p, c.c_int32]),
         "lbm_get_stream": (c.c_int, [c.c_void_p, P(c.c_void_p)]),
@@ -279,6 +280,12 @@ class Lattice:
         u = np.empty((sz, sy, sx, 3), np.float64) if u_out is None else u_out
         self._check(_lib.lbm_get_macroscopic(self._ctx, _ptr(rho), _ptr(u)))
         return rho, u
+
+    def total_mass(self) -> float:
+        """Sum of rho over all fluid cells of the whole lattice (a collective across ranks)."""
+        m = ctypes.c_double()
+        self._check(_lib.lbm_total_mass(self._ctx, ctypes.byref(m)))
+        return m.value
 
     def info(self) -> dict:
         info = LbmInfo()

@@ -29,6 +29,7 @@ def main():
     fl = inputs.add_obstacles(fl, 0.03, seed=13)
     ok = True
     results = {}
+    masses = {}
     # (prec, overlap, layout, exchange): AB uses the fused sweep + NVLink peer stores
     # by default; "nccl" forces pack -> NCCL -> unpack (LBM_EXCHANGE=nccl)
     # plus process grids that split x (the driver's 8-GPU run is 2x2x2)
@@ -67,6 +68,7 @@ def main():
             L.set_pdfs(f0)
             L.step(steps)
             mine = (L.owned_lo, L.owned_hi, L.get_pdfs())
+            mass = L.total_mass()  # collective: every rank calls it
             info = L.info()
             L.close()
             parts = [None] * world
@@ -76,6 +78,7 @@ def main():
                 for lo, hi, a in parts:
                     full[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = a
                 results[(prec, overlap, layout, exch, tuple(pgrid))] = full
+                masses[(prec, overlap, layout, exch, tuple(pgrid))] = mass
                 assert info["exchange_fused"] == (1 if exch.startswith("fused") else 0), info["exchange_fused"]
                 # 8+ patches per rank: same-GPU neighbours take the direct ghost stores
                 assert info["local_direct"] == (0 if exch == "fused_copies" else 1), info
@@ -92,15 +95,17 @@ def main():
                 L.set_pdfs(inputs.noise_pdfs(domain))
                 L.step(steps)
                 single = L.get_pdfs()
+                single_mass = L.total_mass()
             for (p2, overlap, layout, exch, pgrid), res in results.items():
                 if p2 != prec:
                     continue
                 same = np.array_equal(res, single)
+                dm = abs(masses[(p2, overlap, layout, exch, pgrid)] - single_mass)
                 err = float(np.abs(res[mask] - ref[mask]).max())
                 tol = 1e-12 if prec == 8 else 1e-5
                 print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} grid={pgrid} bitwise_vs_1gpu={same} "
-                      f"max|oracle diff|={err:.3e}", flush=True)
-                ok = ok and same and err <= tol
+                      f"max|oracle diff|={err:.3e} |total mass - 1 GPU|={dm:.1e}", flush=True)
+                ok = ok and same and err <= tol and dm <= 1e-9
     flag = torch.tensor([1 if ok else 0])
     dist.broadcast(flag, 0)
     dist.destroy_process_group()

@@ -57,3 +57,34 @@ def test_shear_wave_viscosity_on_gpu(prec, layout):
     amp = 2.0 / N * np.sum(u[:, 0, 0, 0] * np.sin(2 * np.pi * z / N))
     nu = (1.0 / omega - 0.5) / 3.0
     assert amp == pytest.approx(A * np.exp(-nu * (2 * np.pi / N) ** 2 * T), rel=0.015)
+
+
+@pytest.mark.parametrize("prec,layout", [(8, "ab"), (8, "aa"), (4, "ab")])
+def test_total_mass_conserved_and_matches_inputs(prec, layout):
+    """lbm_total_mass: equals N_fluid + sum of the input f~ right after set_pdfs,
+    is conserved by collision + bounce-back in the closed lid-driven cavity
+     over 400 steps (and an odd AA step count), and equals the
+    oracle's sum of rho after 20 steps."""
+    import oracle
+    from paper_1007_1388_b200 import lbm
+    n = (40, 36, 32)
+    fl, wu = inputs.ldc_flags(n)
+    fl = inputs.add_obstacles(fl, 0.03, seed=59)
+    f0 = inputs.noise_pdfs(n, seed=61)
+    fluid = fl[1:-1, 1:-1, 1:-1] == 0
+    m0 = float(fluid.sum()) + float(f0[fluid].sum())
+    L = lbm.Lattice(n, (20, 18, 16), inputs.LDC_OMEGA, prec,
+                    layout=lbm.LBM_LAYOUT_AA if layout == "aa" else lbm.LBM_LAYOUT_AB)
+    try:
+        L.set_flags(fl, wu)
+        L.set_pdfs(f0)
+        assert abs(L.total_mass() - m0) <= 1e-9
+        L.step(20)
+        ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 20, nthreads=oracle.max_threads())
+        m_or = float(fluid.sum()) + float(ref[fluid].sum())
+        tol = 1e-9 if prec == 8 else 1e-3
+        assert abs(L.total_mass() - m_or) <= tol
+        L.step(381)  # odd total: AA streamed representation
+        assert abs(L.total_mass() - m0) <= (1e-9 if prec == 8 else 1e-2)
+    finally:
+        L.close()
