@@ -14,10 +14,13 @@
  *     collide   f~_i(x) <- p_i - omega (p_i - f~eq_i(drho, u))           (eq:lbm P:410-415)
  *               f~eq_i = w_i [drho + rho0 (3 e_i.u + 4.5 (e_i.u)^2 - 1.5 u.u)]  (eq:feq P:416-425)
  *   with centred PDFs f~_i = f_i - w_i rho0, rho0 = 1, two PDF
- *   grids, then the ghost layers of every patch (the paper's Block,
- *   P:209-219) are refreshed: 5 PDFs per face cell, 1 PDF per edge cell, no
- *   corners -- by device copies between patches on the
- *   same GPU and by NCCL send/recv between GPUs.
+ *   grids or one (AA pattern), then the ghost layers of every patch
+ *   (the paper's Block) are refreshed: 5 PDFs per face cell, 1 PDF
+ *   per edge cell, no corners.  By default the sweep
+ *   itself stores those PDFs into the neighbour patches' ghost layers: plain
+ *   stores on the same GPU, NVLink stores into the peer's CUDA-IPC-mapped grid
+ *   across GPUs (one epoch handshake per step); alternatively pack -> NCCL
+ *   send/recv -> unpack.
  *
  * Direction order (ABI, R2):
  *   i : 0      1  2  3  4  5  6   7      8      9      10     11     12     13     14     15     16     17     18
@@ -92,7 +95,8 @@ enum {
 
 /* Exchange transport for neighbouring patches.                               */
 enum {
-    LBM_EXCHANGE_AUTO = 0,        /* same GPU: direct ghost copy; other GPU: NCCL      */
+    LBM_EXCHANGE_AUTO = 0,        /* direct ghost stores by the sweep (same GPU and, over
+                                     NVLink, other GPUs); env LBM_EXCHANGE=nccl: NCCL  */
     LBM_EXCHANGE_FORCE_BUFFERS = 1 /* same-GPU neighbours also go pack -> buffer -> unpack
                                      (exercises the remote path on one GPU; tests)  */
 };
@@ -111,8 +115,9 @@ typedef struct {
     const void *nccl_unique_id; /* LBM_NCCL_ID_BYTES from lbm_nccl_unique_id on rank 0,
                                    same bytes on every rank; required iff nranks > 1            */
     int32_t exchange_mode;  /* LBM_EXCHANGE_*                                                    */
-    int32_t overlap;        /* 1 = sweep patch shells first, exchange on a second stream while
-                               the interiors are swept (multi-GPU); 0 = sequential              */
+    int32_t overlap;        /* NCCL exchange: 1 = sweep patch shells first, exchange on a second
+                               stream while the interiors are swept; 0 = sequential.  (The
+                               fused exchange always sweeps remote shells on its own stream.) */
     int32_t use_graphs;     /* 1 = capture the step pair in a CUDA graph and replay it          */
     void *stream;           /* cudaStream_t for all compute launches; NULL = library-owned      */
     int32_t layout;         /* LBM_LAYOUT_AB or LBM_LAYOUT_AA                                    */
@@ -133,7 +138,8 @@ typedef struct {
     int64_t steps_done;
     double bytes_per_step_algorithmic;     /* 2 * 19 * sizeof(real) * fluid_cells_local   */
     int64_t halo_bytes_remote_per_step;    /* bytes this rank sends to other ranks / step   */
-    int64_t halo_bytes_local_per_step;     /* bytes copied between same-GPU patches / step  */
+    int64_t halo_bytes_local_per_step;     /* bytes exchanged between same-GPU patches / step
+                                              (direct stores or copies)                     */
     int64_t kernel_launches;               /* cumulative library kernel launches            */
     int64_t device_bytes;                  /* device memory held by the ctx                 */
     /* Phase timing (lbm_set_timing): accumulated milliseconds and event counts.
