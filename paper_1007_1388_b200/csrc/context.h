@@ -222,6 +222,25 @@ lbm_status dev_alloc(lbm_ctx *ctx, T **p, size_t bytes)
     return LBM_OK;
 }
 
+// Host -> device uploads and memsets ordered with the ctx stream.  A plain
+// cudaMemcpy from pageable host memory may return before its DMA has landed,
+// and cudaMemset on device memory is asynchronous -- both on the legacy stream,
+// which the library's non-blocking streams do not wait for: a kernel launched
+// right after could read the buffer half written (seen: lid-plane flags).
+inline cudaError_t upload(lbm_ctx *ctx, void *dst, const void *src, size_t bytes)
+{
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e;
+}
+
+inline cudaError_t memset_sync(lbm_ctx *ctx, void *dst, int value, size_t bytes)
+{
+    cudaError_t e = cudaMemsetAsync(dst, value, bytes, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e;
+}
+
 extern thread_local std::string g_create_error;  // api.cu: lbm_last_error(NULL)
 
 Geom make_geom(const int n[3], int esize, int align);

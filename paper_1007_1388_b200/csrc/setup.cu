@@ -62,8 +62,8 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
     if (st) return st;
     st = dev_alloc(ctx, &out.prefix, prefix.size() * sizeof(int64_t));
     if (st) return st;
-    CK(cudaMemcpy(out.boxes, boxes.data(), boxes.size() * sizeof(Box), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(out.prefix, prefix.data(), prefix.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(upload(ctx, out.boxes, boxes.data(), boxes.size() * sizeof(Box)));
+    CK(upload(ctx, out.prefix, prefix.data(), prefix.size() * sizeof(int64_t)));
     return LBM_OK;
 }
 
@@ -92,7 +92,7 @@ lbm_status upload_segs(lbm_ctx *ctx, const std::vector<CopySeg> &v, DevSegs &out
     if (v.empty()) return LBM_OK;
     lbm_status st = dev_alloc(ctx, &out.segs, v.size() * sizeof(CopySeg));
     if (st) return st;
-    CK(cudaMemcpy(out.segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+    CK(upload(ctx, out.segs, v.data(), v.size() * sizeof(CopySeg)));
     return LBM_OK;
 }
 
@@ -250,7 +250,7 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
             if (v.empty() || !dv[j]->segs) continue;
             for (CopySeg &c : v)
                 if (!c.dst_is_buf) c.mask = all_fluid(c) ? 1 : 0;
-            CK(cudaMemcpy(dv[j]->segs, v.data(), v.size() * sizeof(CopySeg), cudaMemcpyHostToDevice));
+            CK(upload(ctx, dv[j]->segs, v.data(), v.size() * sizeof(CopySeg)));
         }
     }
     return LBM_OK;
@@ -362,7 +362,7 @@ lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u,
     uint8_t *dflags = nullptr;
     lbm_status st = dev_alloc(ctx, &dflags, total);
     if (st) return st;
-    cudaError_t e = cudaMemcpy(dflags, flags, total, cudaMemcpyHostToDevice);
+    cudaError_t e = upload(ctx, dflags, flags, total);
     if (e == cudaSuccess)
         e = launch_build_flags(dflags, ctx->dec.domain, ctx->dec.periodic, ctx->d_origin, ctx->dec.nlocal, ctx->g,
                                ctx->flags, ctx->kind, ctx->stream);
@@ -380,10 +380,10 @@ lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u,
             cd[(size_t)k * Q + i] = 6.0 * WQ(i) * 1.0 * eu;
         }
     if (ctx->esize == 8) {
-        CK(cudaMemcpy(ctx->corr, cd.data(), cd.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CK(upload(ctx, ctx->corr, cd.data(), cd.size() * sizeof(double)));
     } else {
         std::vector<float> cf(cd.begin(), cd.end());
-        CK(cudaMemcpy(ctx->corr, cf.data(), cf.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CK(upload(ctx, ctx->corr, cf.data(), cf.size() * sizeof(float)));
     }
     {
         lbm_status st2 = update_seg_masks(ctx, flags);
@@ -489,9 +489,9 @@ lbm_status setup_direct(lbm_ctx *ctx)
     if ((st = dev_alloc(ctx, &ctx->d_epoch, sizeof(unsigned long long)))) return st;
     if ((st = dev_alloc(ctx, &ctx->d_inbox, (size_t)R * sizeof(unsigned long long)))) return st;
     if ((st = dev_alloc(ctx, &ctx->d_error, sizeof(int)))) return st;
-    CK(cudaMemset(ctx->d_epoch, 0, sizeof(unsigned long long)));
-    CK(cudaMemset(ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
-    CK(cudaMemset(ctx->d_error, 0, sizeof(int)));
+    CK(memset_sync(ctx, ctx->d_epoch, 0, sizeof(unsigned long long)));
+    CK(memset_sync(ctx, ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
+    CK(memset_sync(ctx, ctx->d_error, 0, sizeof(int)));
     // Remote peers of the exchange plan.
     std::vector<int> peers;
     for (const Peer &p : ctx->ex[EX_AB].peers)
@@ -509,7 +509,7 @@ lbm_status setup_direct(lbm_ctx *ctx)
         CK(cudaIpcGetMemHandle(&mine[2], ctx->d_inbox));
         char *dbuf = nullptr;
         if ((st = dev_alloc(ctx, &dbuf, 3 * hb * (size_t)(R + 1)))) return st;
-        CK(cudaMemcpy(dbuf, mine.data(), 3 * hb, cudaMemcpyHostToDevice));
+        CK(upload(ctx, dbuf, mine.data(), 3 * hb));
         NK(ncclAllGather(dbuf, dbuf + 3 * hb, 3 * hb, ncclUint8, ctx->nccl, ctx->stream));
         std::vector<cudaIpcMemHandle_t> all((size_t)3 * R);
         CK(cudaMemcpyAsync(all.data(), dbuf + 3 * hb, 3 * hb * R, cudaMemcpyDeviceToHost, ctx->stream));
@@ -539,7 +539,7 @@ lbm_status setup_direct(lbm_ctx *ctx)
         // every rank must take the same path
         int *dok = nullptr;
         if ((st = dev_alloc(ctx, &dok, sizeof(int)))) return st;
-        CK(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+        CK(upload(ctx, dok, &ok, sizeof(int)));
         NK(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, ctx->nccl, ctx->stream));
         CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -566,7 +566,7 @@ lbm_status setup_direct(lbm_ctx *ctx)
     }
     ctx->h_nbr = nbr;
     if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
-    CK(cudaMemcpy(ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *), cudaMemcpyHostToDevice));
+    CK(upload(ctx, ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *)));
     std::vector<unsigned long long *> pin;
     std::vector<int> prank;
     for (int r : peers) {
@@ -576,9 +576,9 @@ lbm_status setup_direct(lbm_ctx *ctx)
     ctx->npeers_direct = (int)peers.size();
     if (!peers.empty()) {
         if ((st = dev_alloc(ctx, &ctx->d_peer_inbox, pin.size() * sizeof(void *)))) return st;
-        CK(cudaMemcpy(ctx->d_peer_inbox, pin.data(), pin.size() * sizeof(void *), cudaMemcpyHostToDevice));
+        CK(upload(ctx, ctx->d_peer_inbox, pin.data(), pin.size() * sizeof(void *)));
         if ((st = dev_alloc(ctx, &ctx->d_peer_rank, prank.size() * sizeof(int)))) return st;
-        CK(cudaMemcpy(ctx->d_peer_rank, prank.data(), prank.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(upload(ctx, ctx->d_peer_rank, prank.data(), prank.size() * sizeof(int)));
     }
     ctx->direct = true;
     return LBM_OK;
@@ -730,7 +730,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             for (int a = 0; a < 3; ++a) origin[3 * l + a] = c[a] * dec.patch[a];
         }
         if ((st = dev_alloc(ctx, &ctx->d_origin, origin.size() * sizeof(int)))) return bail(st);
-        if (cudaMemcpy(ctx->d_origin, origin.data(), origin.size() * sizeof(int), cudaMemcpyHostToDevice) !=
+        if (upload(ctx, ctx->d_origin, origin.data(), origin.size() * sizeof(int)) !=
             cudaSuccess)
             return bail(LBM_ERR_CUDA);
     }
@@ -802,7 +802,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
                 }
             }
             if ((st = dev_alloc(ctx, &ctx->d_lnbr, tab.size() * sizeof(void *)))) return bail(st);
-            if (cudaMemcpy(ctx->d_lnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+            if (upload(ctx, ctx->d_lnbr, tab.data(), tab.size() * sizeof(void *)) !=
                 cudaSuccess)
                 return bail(LBM_ERR_CUDA);
             ctx->lpull = true;
@@ -838,7 +838,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
                 }
             }
             if ((st = dev_alloc(ctx, &ctx->d_dnbr, tab.size() * sizeof(void *)))) return bail(st);
-            if (cudaMemcpy(ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *), cudaMemcpyHostToDevice) !=
+            if (upload(ctx, ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *)) !=
                 cudaSuccess)
                 return bail(LBM_ERR_CUDA);
             ctx->ldirect = want_local;

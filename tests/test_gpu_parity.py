@@ -312,3 +312,34 @@ def test_local_direct_equals_ghost_copies(prec, n, patch, periodic, monkeypatch)
     np.testing.assert_array_equal(out["1"], one)
     ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 11, periodic=periodic, nthreads=oracle.max_threads())
     assert max_fluid_diff(out["1"], ref, fl) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", [4, 8])
+def test_patch_heavy_128_in_8_patches(prec):
+    """SURVEY 8(d) config 5 parity: LDC 128^3 in 8 patches of 64^3 on one GPU
+    (direct ghost stores between them) after 100 steps -- against the oracle
+    and bitwise against one 128^3 patch."""
+    n = (128, 128, 128)
+    fl, wu = inputs.ldc_flags(n)
+    f0 = inputs.noise_pdfs(n)
+    patched = run_gpu(n, fl, wu, f0, 100, prec, patch=(64, 64, 64))
+    single = run_gpu(n, fl, wu, f0, 100, prec)
+    np.testing.assert_array_equal(patched, single)
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 100, nthreads=oracle.max_threads())
+    assert max_fluid_diff(patched, ref, fl) <= TOL[prec]
+
+
+def test_flags_upload_complete_at_size():
+    """Regression: the flag upload is ordered with the
+    library's stream -- a plain cudaMemcpy from pageable memory returned before
+    its DMA landed and the lid plane was sometimes read as fluid.  Repeated
+    set_flags / get_flags at 160^3 must read back exactly (the 128^3 parity
+    test above checks the resulting dynamics)."""
+    m = lbm()
+    n = (160, 160, 160)
+    fl, wu = inputs.ldc_flags(n)
+    for prec in (4, 8):
+        for _ in range(4):
+            with m.Lattice(n, n, inputs.LDC_OMEGA, prec) as L:
+                L.set_flags(fl, wu)
+                np.testing.assert_array_equal(L.get_flags(), fl)
