@@ -159,6 +159,99 @@ void run4(int n, int P)
     cudaFree(b);
 }
 
+// Patch layout with the x-ghost columns moved out of the rows (a design study for
+// the patch-heavy configuration): rows hold exactly the n interior cells (aligned,
+// pitch n, no x padding), and each patch keeps two compact arrays g[side][5 q][z][y]
+// for its x ghosts.  The pull of the 10 e_x != 0 directions takes the row values
+// and, for the cell on the patch's x face, the compact ghost; every cell on an x
+// face also writes its 5 outgoing values into the compact array (the neighbour's
+// ghost).  Two cells per thread, block (32, 4) = 64 x 4.
+template <typename T>
+__global__ void __launch_bounds__(128, 3) stream_compact_kernel(const T *__restrict__ src, T *__restrict__ dst,
+                                                               const T *__restrict__ gsrc, T *__restrict__ gdst,
+                                                               int n, long long plane, long long qs)
+{
+    const int x0 = blockIdx.x * 64 + 2 * threadIdx.x;
+    const int y = blockIdx.y * 4 + threadIdx.y;
+    const int z = blockIdx.z % n;
+    const long long p = blockIdx.z / n;
+    if (x0 >= n || y >= n) return;
+    const long long pbase = p * Q * qs;
+    const long long cell = pbase + ((long long)(z + 1) * (n + 2) + (y + 1)) * n + x0;  // rows: pitch n
+    const long long gplane = (long long)(n + 2) * (n + 2);                              // [z][y] with halo
+    const long long gbase = p * 2 * 5 * gplane;                                          // [side][5][z][y]
+    T a[Q], b[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        const long long sh = cEY[i] * (long long)n + cEZ[i] * plane;  // y / z shift only
+        const T *row = src + cell + i * qs - sh;
+        if (cEX[i] == 0) {
+            a[i] = __ldg(row);
+            b[i] = __ldg(row + 1);
+        } else if (cEX[i] > 0) {  // pull from x - 1
+            const long long gi = gbase + (0 * 5 + (i % 5)) * gplane + (long long)(z + 1 - cEZ[i]) * (n + 2) + (y + 1 - cEY[i]);
+            a[i] = x0 == 0 ? __ldg(gsrc + gi) : __ldg(row - 1);
+            b[i] = __ldg(row);
+        } else {                  // pull from x + 1
+            const long long gi = gbase + (1 * 5 + (i % 5)) * gplane + (long long)(z + 1 - cEZ[i]) * (n + 2) + (y + 1 - cEY[i]);
+            a[i] = __ldg(row + 1);
+            b[i] = x0 + 2 >= n ? __ldg(gsrc + gi) : __ldg(row + 2);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        dst[cell + i * qs] = a[i];
+        dst[cell + i * qs + 1] = b[i];
+    }
+    // x-face cells write their 5 outgoing values into the compact ghost arrays
+    if (x0 == 0 || x0 + 2 >= n) {
+        const long long go = (long long)(z + 1) * (n + 2) + (y + 1);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            if (x0 == 0) gdst[gbase + (1 * 5 + k) * gplane + go] = a[2 * k + 2];
+            if (x0 + 2 >= n) gdst[gbase + (0 * 5 + k) * gplane + go] = b[2 * k + 1];
+        }
+    }
+}
+
+template <typename T>
+void run_compact(int n, int P)
+{
+    const long long plane = (long long)n * (n + 2), qs = plane * (n + 2);
+    const size_t bytes = (size_t)P * Q * qs * sizeof(T);
+    const size_t gbytes = (size_t)P * 2 * 5 * (n + 2) * (n + 2) * sizeof(T);
+    T *a, *b, *ga, *gb;
+    cudaMalloc(&a, bytes);
+    cudaMalloc(&b, bytes);
+    cudaMalloc(&ga, gbytes);
+    cudaMalloc(&gb, gbytes);
+    cudaMemset(a, 0, bytes);
+    cudaMemset(b, 0, bytes);
+    cudaMemset(ga, 0, gbytes);
+    cudaMemset(gb, 0, gbytes);
+    dim3 grid((n + 63) / 64, (n + 3) / 4, n * P), block(32, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n * P;
+    for (int w = 0; w < 5; ++w) stream_compact_kernel<T><<<grid, block>>>(a, b, ga, gb, n, plane, qs);
+    const int reps = 50;
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r)
+        stream_compact_kernel<T><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, r & 1 ? gb : ga, r & 1 ? ga : gb, n,
+                                                  plane, qs);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("elem=%zu n=%d patches=%d pull-shifted, compact x ghosts (rows unpadded): %.3f ms/launch, %.1f GB/s algorithmic\n",
+           sizeof(T), n, P, ms / reps, alg / (ms / reps * 1e-3) / 1e9);
+    cudaFree(a);
+    cudaFree(b);
+    cudaFree(ga);
+    cudaFree(gb);
+}
+
 template <typename T>
 __global__ void copy1d(const T *__restrict__ s, T *__restrict__ d, long long n)
 {
@@ -228,5 +321,9 @@ int main(int argc, char **argv)
     run<double>(n, P);
     run<float>(n, P);
     run4(n, P);
+    if (P > 1) {
+        run_compact<double>(n, P);
+        run_compact<float>(n, P);
+    }
     return 0;
 }
