@@ -252,6 +252,40 @@ void run_compact(int n, int P)
     cudaFree(gb);
 }
 
+// Layout variant: x = -1 stored in the previous row's tail slot (x = 0 at offset 0,
+// pitch roundup(n + 2, 128 B)), i.e. half the row padding of the default layout.
+template <typename T>
+void run_xo0(int n, int P)
+{
+    const int ae = 128 / sizeof(T), xo = 0;
+    const int px = ((n + 2 + ae - 1) / ae) * ae;
+    const long long plane = (long long)px * (n + 2), qs = plane * (n + 2);
+    const size_t elems = (size_t)P * Q * qs + 2 * px;
+    T *a0, *b0;
+    cudaMalloc(&a0, elems * sizeof(T));
+    cudaMalloc(&b0, elems * sizeof(T));
+    cudaMemset(a0, 0, elems * sizeof(T));
+    cudaMemset(b0, 0, elems * sizeof(T));
+    T *a = a0 + px, *b = b0 + px;  // room for x = -1 of the very first row
+    dim3 grid((n + 63) / 64, (n + 3) / 4, n * P), block(32, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const double alg = 2.0 * Q * sizeof(T) * (double)n * n * n * P;
+    for (int w = 0; w < 5; ++w) stream_kernel<T, 1><<<grid, block>>>(a, b, n, px, plane, qs, xo);
+    const int reps = 50;
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) stream_kernel<T, 1><<<grid, block>>>(r & 1 ? b : a, r & 1 ? a : b, n, px, plane, qs, xo);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("elem=%zu n=%d patches=%d pull-shifted, x = -1 in the previous row (pitch %d): %.3f ms/launch, %.1f GB/s algorithmic\n",
+           sizeof(T), n, P, px, ms / reps, alg / (ms / reps * 1e-3) / 1e9);
+    cudaFree(a0);
+    cudaFree(b0);
+}
+
 template <typename T>
 __global__ void copy1d(const T *__restrict__ s, T *__restrict__ d, long long n)
 {
@@ -325,5 +359,7 @@ int main(int argc, char **argv)
         run_compact<double>(n, P);
         run_compact<float>(n, P);
     }
+    run_xo0<double>(n, P);
+    run_xo0<float>(n, P);
     return 0;
 }
