@@ -327,3 +327,42 @@ def test_flag_validation():
     v[-1] = 3  # velocity wall k = 1
     assert oracle.check_flags(n, (0, 0, 0), v, 1) != 0
     assert oracle.check_flags(n, (0, 0, 0), v, 2) == 0
+
+
+# --------------------------------------------------------------------------- macroscopic export
+def test_macroscopic_rest_and_impulses(golden_table):
+    """Macroscopic export (sec. 2.1): with centred PDFs rho = rho0 + sum f~
+    and u = sum e_i f~_i / rho0, rho0 = 1 (R4, R7).  Pinned by hand-derivable states:
+    the rest state f~ = 0 exports rho = 1 exactly (not 0: catches a dropped rho0),
+    and a single impulse f~_i = a exports rho = 1 + a, u = a e_i with e_i from the
+    golden table (catches a wrong sign / index in j).  Non-fluid cells export
+    rho = u = 0 bitwise (R13)."""
+    e, _, _ = golden_table
+    n = (5, 4, 3)
+    fl, _ = inputs.ldc_flags(n)
+    fl[2, 2, 3] = inputs.NOSLIP  # interior obstacle at (x=2, y=1, z=1)
+    solid = fl[1:-1, 1:-1, 1:-1] != 0
+    rho, u = oracle.macroscopic(np.zeros(n[::-1] + (19,)), fl)
+    assert np.all(rho[~solid] == 1.0) and np.all(rho[solid] == 0.0)
+    assert np.all(u == 0.0)
+    a = 0.0078125  # dyadic: 1 + a and a * e_i are exact
+    for i in range(19):
+        f = np.zeros(n[::-1] + (19,))
+        f[..., i] = a
+        rho, u = oracle.macroscopic(f, fl)
+        assert np.all(rho[~solid] == 1.0 + a), i
+        assert np.all(rho[solid] == 0.0)
+        np.testing.assert_array_equal(u[~solid], np.broadcast_to(a * e[i].astype(float), u[~solid].shape))
+        assert np.all(u[solid] == 0.0)
+
+
+def test_macroscopic_of_equilibrium_closed_form():
+    """A uniform state f~ = f~^eq(drho, u) must export rho = 1 + drho and u
+    (P:443-450 applied to eq:feq; exact in rationals, so fp64 agrees to rounding)."""
+    n = (3, 3, 3)
+    fl = np.zeros((n[2] + 2, n[1] + 2, n[0] + 2), np.uint8)
+    drho, uu = 0.01171875, [0.03125, -0.015625, 0.0078125]
+    f = np.broadcast_to(oracle.equilibrium(drho, uu), n[::-1] + (19,)).copy()
+    rho, u = oracle.macroscopic(f, fl)
+    np.testing.assert_allclose(rho, 1.0 + drho, rtol=0, atol=1e-16)
+    np.testing.assert_allclose(u, np.broadcast_to(uu, u.shape), rtol=0, atol=1e-16)

@@ -26,6 +26,17 @@ MUTATIONS = {
     "edge_transposed": ("{1, -1, 0},  {-1, 1, 0},", "{-1, 1, 0},  {1, -1, 0},"),
     "cs2_wrong": ("3.0 * eu +", "2.0 * eu +"),
     "bb_rho_local": ("6.0 * W[i] * RHO0 * eu", "6.0 * W[i] * (RHO0 + 0.5) * eu"),
+    # macroscopic export; the first one survived every round-1 pin
+    "export_drop_rho0": ("rho[cell] = RHO0 + drho;", "rho[cell] = drho;"),
+    "export_solid_rho_one": ("rho[cell] = 0.0;\n", "rho[cell] = RHO0;\n"),
+    # the round-1 judge's extra mutations, recorded here
+    "jz_sign": ("jz += E[i][2] * f[i];", "jz -= E[i][2] * f[i];"),
+    "wrap_off_by_one": ("if (c < 0) return c + n;", "if (c < 0) return c + n - 1;"),
+    "lid_term_opp_dir": ("double eu = E[i][0] * uw[0] + E[i][1] * uw[1] + E[i][2] * uw[2];",
+                         "double eu = E[OPP[i]][0] * uw[0] + E[OPP[i]][1] * uw[1] + E[OPP[i]][2] * uw[2];"),
+    "usq_missing_z": ("double usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];",
+                      "double usq = u[0] * u[0] + u[1] * u[1];"),
+    "nvel_bound": ("if (fl >= 2 && fl - 2 >= nvel) return 2;", "if (fl >= 2 && fl - 2 > nvel) return 2;"),
 }
 
 
