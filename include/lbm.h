@@ -97,8 +97,16 @@ enum {
 enum {
     LBM_EXCHANGE_AUTO = 0,        /* direct ghost stores by the sweep (same GPU and, over
                                      NVLink, other GPUs); env LBM_EXCHANGE=nccl: NCCL  */
-    LBM_EXCHANGE_FORCE_BUFFERS = 1 /* same-GPU neighbours also go pack -> buffer -> unpack
-                                     (exercises the remote path on one GPU; tests)  */
+    LBM_EXCHANGE_FORCE_BUFFERS = 1, /* every neighbour patch, same-GPU ones included, goes
+                                     pack -> buffer -> grouped ncclSend/ncclRecv -> unpack
+                                     (P:287-313), shells first and overlapped with the
+                                     interiors when overlap = 1; on one GPU through a
+                                     one-rank communicator (the NCCL path, tested there) */
+    LBM_EXCHANGE_SELF_PEER = 2     /* nranks == 1 only: every neighbour patch is reached as
+                                     if on another GPU that is this one -- remote shells
+                                     on the comm stream with direct stores through the
+                                     peer table, one epoch handshake per step (the fused
+                                     multi-GPU path, tested on one GPU)              */
 };
 
 /* Extended creation parameters (lbm_config_default fills the defaults).     */
@@ -147,8 +155,9 @@ typedef struct {
        4 nccl  5 unpack  6 step total  7 reserved                                        */
     double phase_ms[LBM_NPHASES];
     int64_t phase_count[LBM_NPHASES];
-    int64_t row_pitch_elems;               /* x pitch of a patch row (padding / alignment)  */
-    int32_t align_bytes;                   /* alignment of interior x = 0                   */
+    int64_t row_pitch_elems;               /* PDF row pitch: n_x rounded up to a 32-B sector
+                                              (x ghosts live in compact side columns)       */
+    int32_t align_bytes;                   /* alignment of every row start (32)             */
     int32_t graphs_active;
     int32_t layout;                        /* LBM_LAYOUT_*                                  */
     int32_t aa_phase;                      /* AA: 0 swapped (even step count), 1 streamed   */
@@ -157,11 +166,18 @@ typedef struct {
                                               other GPUs: NVLink stores to CUDA-IPC-mapped
                                               memory, one epoch handshake per step);
                                               0: pack -> NCCL / copy -> unpack             */
-    int32_t local_pull;                    /* 1: face cells read same-GPU neighbour patches
-                                              directly (no ghost copies between them)      */
+    int32_t local_pull;                    /* always 0 (the round-1 local-pull sweep was
+                                              measured slower and removed)                 */
     int32_t local_direct;                  /* 1: the sweep stores the outgoing PDFs of face /
                                               edge cells straight into same-GPU neighbour
                                               patches' ghost layers (no ghost copies)     */
+    int32_t overlap_active;                /* 1: buffered exchange with shells first and the
+                                              transport overlapped with the interior sweep */
+    int32_t nccl_ranks;                    /* size of the ctx's NCCL communicator (0: none;
+                                              1: one-GPU FORCE_BUFFERS self-peer messages)  */
+    int32_t fused_peers;                   /* peers of the fused exchange's epoch handshake
+                                              (SELF_PEER on one GPU: 1, this rank)          */
+    int32_t reserved0;
 } lbm_info;
 
 /* One remote message of the static exchange plan (lbm_plan, host-only).      */

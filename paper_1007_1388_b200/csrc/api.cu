@@ -8,6 +8,16 @@
 
 namespace lbm {
 thread_local std::string g_create_error;
+
+// Before the host reads or replaces the state: drain both streams and, with the
+// fused exchange, wait until the peers' last stores into this rank's grid have
+// landed (quiesce, step.cu).
+static lbm_status drain(lbm_ctx *ctx)
+{
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->comm_stream));
+    return quiesce(ctx);
+}
 }  // namespace lbm
 
 // ===================================================================== C ABI
@@ -64,8 +74,9 @@ LBM_API lbm_status lbm_set_flags(lbm_ctx *ctx, const uint8_t *flags, const doubl
     if (m[0]) return ctx->fail(LBM_ERR_ARG, m);
     if (ctx->layout == LBM_LAYOUT_AA && ctx->aa_phase != 0)
         return ctx->fail(LBM_ERR_STATE, "AA layout: set_flags is only valid after an even number of steps");
-    CK(cudaStreamSynchronize(ctx->stream));
-    lbm_status st = apply_flags(ctx, flags, wall_u, nvel);
+    lbm_status st = drain(ctx);
+    if (st) return st;
+    st = apply_flags(ctx, flags, wall_u, nvel);
     if (st) return st;
     return refresh_state(ctx);
 }
@@ -74,7 +85,10 @@ LBM_API lbm_status lbm_get_flags(lbm_ctx *ctx, uint8_t *out)
 {
     CHECK_CTX(ctx);
     if (!out) return ctx->fail(LBM_ERR_ARG, "flags_out is NULL");
-    CK(cudaStreamSynchronize(ctx->stream));
+    {
+        lbm_status st = drain(ctx);
+        if (st) return st;
+    }
     const Decomp &d = ctx->dec;
     const Geom &g = ctx->g;
     std::vector<uint8_t> h((size_t)d.nlocal * g.fs);
@@ -91,7 +105,7 @@ LBM_API lbm_status lbm_get_flags(lbm_ctx *ctx, uint8_t *out)
                     lc[a] = (int)(c[a] - (int64_t)b[a] * g.n[a]);
                 }
                 const int lp = (b[2] * d.brick[1] + b[1]) * d.brick[0] + b[0];
-                const int64_t ci = ((int64_t)(lc[2] + 1) * g.py + (lc[1] + 1)) * g.px + (lc[0] + g.xo);
+                const int64_t ci = flag_index(g, lc[0], lc[1], lc[2]);
                 out[((z + 1) * (on[1] + 2) + (y + 1)) * (on[0] + 2) + (x + 1)] = h[(size_t)lp * g.fs + ci];
             }
     return LBM_OK;
@@ -101,8 +115,9 @@ LBM_API lbm_status lbm_set_pdfs(lbm_ctx *ctx, const double *f)
 {
     CHECK_CTX(ctx);
     if (!f) return ctx->fail(LBM_ERR_ARG, "f is NULL");
-    CK(cudaStreamSynchronize(ctx->stream));
-    lbm_status st = transfer_chunks(ctx, const_cast<double *>(f), true, 0, nullptr, nullptr);
+    lbm_status st = drain(ctx);
+    if (st) return st;
+    st = transfer_chunks(ctx, const_cast<double *>(f), true, 0, nullptr, nullptr);
     if (st) return st;
     return refresh_state(ctx);
 }
@@ -110,6 +125,10 @@ LBM_API lbm_status lbm_set_pdfs(lbm_ctx *ctx, const double *f)
 LBM_API lbm_status lbm_init_noise(lbm_ctx *ctx, uint64_t seed)
 {
     CHECK_CTX(ctx);
+    {
+        lbm_status st = drain(ctx);
+        if (st) return st;
+    }
     const Decomp &d = ctx->dec;
     const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
     cudaError_t e = ctx->esize == 8
@@ -133,13 +152,10 @@ LBM_API lbm_status lbm_step_async(lbm_ctx *ctx, int64_t nsteps)
 LBM_API lbm_status lbm_synchronize(lbm_ctx *ctx)
 {
     CHECK_CTX(ctx);
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaStreamSynchronize(ctx->comm_stream));
-    if (ctx->d_error && ctx->npeers_direct > 0) {
-        int err = 0;
-        CK(cudaMemcpy(&err, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
-        if (err) return ctx->fail(LBM_ERR_INTERNAL, "fused exchange: a peer GPU did not reach the step barrier within LBM_PEER_TIMEOUT_S (default 120 s)");
-    }
+    // lbm_step returns with the state globally quiescent: the peers' stores
+    // into this rank's grid for every step done have landed.
+    lbm_status st = drain(ctx);
+    if (st) return st;
     if (ctx->timing) return flush_timing(ctx);
     return LBM_OK;
 }
@@ -155,7 +171,8 @@ LBM_API lbm_status lbm_get_pdfs(lbm_ctx *ctx, double *f_out)
 {
     CHECK_CTX(ctx);
     if (!f_out) return ctx->fail(LBM_ERR_ARG, "f_out is NULL");
-    CK(cudaStreamSynchronize(ctx->stream));
+    lbm_status st = drain(ctx);
+    if (st) return st;
     return transfer_chunks(ctx, f_out, false, 0, nullptr, nullptr);
 }
 
@@ -164,6 +181,10 @@ LBM_API lbm_status lbm_get_pdfs_at(lbm_ctx *ctx, const int64_t *xyz, int64_t n, 
     CHECK_CTX(ctx);
     if (n < 0 || (n > 0 && (!xyz || !out))) return ctx->fail(LBM_ERR_ARG, "bad sample arguments");
     if (n == 0) return LBM_OK;
+    {
+        lbm_status st = drain(ctx);
+        if (st) return st;
+    }
     std::vector<int64_t> loc((size_t)3 * n);
     for (int64_t k = 0; k < n; ++k)
         for (int a = 0; a < 3; ++a) {
@@ -207,7 +228,10 @@ LBM_API lbm_status lbm_get_pdfs_at(lbm_ctx *ctx, const int64_t *xyz, int64_t n, 
 LBM_API lbm_status lbm_get_macroscopic(lbm_ctx *ctx, double *rho_out, double *u_out)
 {
     CHECK_CTX(ctx);
-    CK(cudaStreamSynchronize(ctx->stream));
+    {
+        lbm_status st = drain(ctx);
+        if (st) return st;
+    }
     if (!rho_out && !u_out) return LBM_OK;
     return transfer_chunks(ctx, nullptr, false, 1, rho_out, u_out);
 }
@@ -216,7 +240,8 @@ LBM_API lbm_status lbm_total_mass(lbm_ctx *ctx, double *mass_out)
 {
     CHECK_CTX(ctx);
     if (!mass_out) return ctx->fail(LBM_ERR_ARG, "mass_out is NULL");
-    lbm_status st;
+    lbm_status st = drain(ctx);
+    if (st) return st;
     if (!ctx->d_mass && (st = dev_alloc(ctx, &ctx->d_mass, (size_t)(kMassBlocks + 1) * sizeof(double)))) return st;
     const Decomp &d = ctx->dec;
     const int64_t on[3] = {d.owned_hi[0] - d.owned_lo[0], d.owned_hi[1] - d.owned_lo[1], d.owned_hi[2] - d.owned_lo[2]};
@@ -288,14 +313,18 @@ LBM_API lbm_status lbm_get_info(lbm_ctx *ctx, lbm_info *out)
         out->phase_count[i] = ctx->phase_count[i];
     }
     out->row_pitch_elems = ctx->g.px;
-    out->align_bytes = ctx->align;
+    out->align_bytes = 32;  // rows start on 32-B sectors
     out->graphs_active = (ctx->graph[0] || ctx->graph[1]) ? 1 : 0;
     out->layout = ctx->layout;
     out->aa_phase = ctx->aa_phase;
     out->exchange_fused = ctx->direct ? 1 : 0;
-    out->local_pull = ctx->lpull ? 1 : 0;
+    out->local_pull = 0;  // removed in round 2 (measured slower)
     out->local_direct = ctx->ldirect ? 1 : 0;
-    if (ctx->lpull) out->halo_bytes_local_per_step = 0;
+    out->overlap_active = (ctx->use_overlap && !ctx->direct) ? 1 : 0;
+    int nr = 0;
+    if (ctx->nccl && ncclCommCount(ctx->nccl, &nr) != ncclSuccess) nr = -1;
+    out->nccl_ranks = nr;
+    out->fused_peers = ctx->direct ? ctx->npeers_direct : 0;
     return LBM_OK;
 }
 

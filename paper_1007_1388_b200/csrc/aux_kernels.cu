@@ -33,24 +33,22 @@ __global__ void __launch_bounds__(256) copy_segments_kernel(const CopySeg *segs,
         if (sg.src_is_buf)
             v = buf_src[sg.src_base + e];
         else
-            v = grid_src[sg.src_base + q * g.qs +
-                         cell_index(g, sg.src_lo[0] + cx, sg.src_lo[1] + cy, sg.src_lo[2] + cz)];
+            v = grid_src[sg.src_base + pdf_index(g, q, sg.src_lo[0] + cx, sg.src_lo[1] + cy, sg.src_lo[2] + cz)];
         if (sg.dst_is_buf) {
             buf_dst[sg.dst_base + e] = v;
         } else {
             const int y[3] = {sg.dst_lo[0] + cx, sg.dst_lo[1] + cy, sg.dst_lo[2] + cz};
-            const int64_t ci = cell_index(g, y[0], y[1], y[2]);
-            bool ok = sg.mask == 1 || flags[sg.dst_flag_base + ci] == 0;  // mask 1: all destinations fluid
+            bool ok = sg.mask == 1 || flags[sg.dst_flag_base + flag_index(g, y[0], y[1], y[2])] == 0;  // mask 1: all destinations fluid
             if (sg.mask == 2 && ok) {
                 // AA half-exchange 2: the value was scattered by the sender's cell
-                // w = y - e_q; only entries whose writer is a fluid cell of the
-                // sender (not another patch's ghost) are delivered.
+                // w = y - e_q; only entries whose writer is a fluid cell of the sender
+                // (not another patch's ghost) are delivered.
                 const int w[3] = {y[0] - EX(q), y[1] - EY(q), y[2] - EZ(q)};
                 for (int a2 = 0; a2 < 3; ++a2)
                     if (sg.d[a2] == 0 && (w[a2] < 0 || w[a2] >= g.n[a2])) ok = false;
-                if (ok) ok = flags[sg.dst_flag_base + cell_index(g, w[0], w[1], w[2])] == 0;
+                if (ok) ok = flags[sg.dst_flag_base + flag_index(g, w[0], w[1], w[2])] == 0;
             }
-            if (ok) grid_dst[sg.dst_base + q * g.qs + ci] = v;
+            if (ok) grid_dst[sg.dst_base + pdf_index(g, q, y[0], y[1], y[2])] = v;
         }
     }
 }
@@ -81,11 +79,11 @@ __global__ void build_flags_kernel(const uint8_t *global, int64_t nx, int64_t ny
     const int64_t n[3] = {nx, ny, nz};
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int col = (int)(e % g.px);
-        const int64_t r = e / g.px;
+        const int col = (int)(e % g.fpx);
+        const int64_t r = e / g.fpx;
         const int row = (int)(r % g.py);
         const int pl = (int)(r / g.py);
-        const int lc[3] = {col - g.xo, row - 1, pl - 1};
+        const int lc[3] = {col - g.fxo, row - 1, pl - 1};
         uint8_t v = 1;
         if (lc[0] >= -1 && lc[0] <= g.n[0]) {
             int64_t c[3];
@@ -103,34 +101,36 @@ __global__ void build_flags_kernel(const uint8_t *global, int64_t nx, int64_t ny
 
 // kind: 2 = non-fluid (or ghost / padding), 1 = fluid with a non-fluid
 // neighbour among the 18 (needs the flag-driven path), 0 = fluid with only
-// fluid neighbours (pure pull).
-__global__ void build_kind_kernel(const Geom g, const uint8_t *flags, uint8_t *kind)
+// fluid neighbours (pure pull).  wmask (kind-1 cells): bit j set if x + e_j is
+// non-fluid -- one 32-bit word instead of 18 flag bytes for the sweep's
+// store-side bounce-back.
+__global__ void build_kind_kernel(const Geom g, const uint8_t *flags, uint8_t *kind, uint32_t *wmask)
 {
     const int lp = blockIdx.y;
     const int64_t total = g.fs;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int col = (int)(e % g.px);
-        const int64_t r = e / g.px;
+        const int col = (int)(e % g.fpx);
+        const int64_t r = e / g.fpx;
         const int row = (int)(r % g.py);
         const int pl = (int)(r / g.py);
-        const int x = col - g.xo, y = row - 1, z = pl - 1;
+        const int x = col - g.fxo, y = row - 1, z = pl - 1;
         const uint8_t *f = flags + (int64_t)lp * g.fs;
         uint8_t kd = 2;
+        uint32_t m = 0;
         if (x >= 0 && x < g.n[0] && y >= 0 && y < g.n[1] && z >= 0 && z < g.n[2] && f[e] == 0) {
-            kd = 0;
-            for (int i = 1; i < Q; ++i) {
-                const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-                if (f[e - sh] != 0) kd = 1;
-            }
+            for (int j = 1; j < Q; ++j)
+                if (f[e + flag_shift(g, j)] != 0) m |= 1u << j;
+            kd = m ? 1 : 0;
         }
         kind[(int64_t)lp * g.fs + e] = kd;
+        wmask[(int64_t)lp * g.fs + e] = m;
     }
 }
 
 cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], const int periodic[3],
                                const int *patch_origin, int nlocal, const Geom &g, uint8_t *flags,
-                               uint8_t *kind, cudaStream_t s)
+                               uint8_t *kind, uint32_t *wmask, cudaStream_t s)
 {
     int64_t bx = (g.fs + 255) / 256;
     if (bx > 4096) bx = 4096;
@@ -145,7 +145,8 @@ cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], c
     for (int off = 0; off < nlocal; off += 65535) {
         int n = nlocal - off < 65535 ? nlocal - off : 65535;
         dim3 grid((unsigned)bx, (unsigned)n);
-        build_kind_kernel<<<grid, 256, 0, s>>>(g, flags + (int64_t)off * g.fs, kind + (int64_t)off * g.fs);
+        build_kind_kernel<<<grid, 256, 0, s>>>(g, flags + (int64_t)off * g.fs, kind + (int64_t)off * g.fs,
+                                               wmask + (int64_t)off * g.fs);
     }
     return cudaGetLastError();
 }
@@ -172,15 +173,16 @@ __device__ __forceinline__ void owned_to_patch(const Geom &g, const int brick[3]
 //          x + e_i the bounced value A[x][opp(i)] minus its wall term).
 __device__ __forceinline__ int rep_slot(int rep, int i) { return rep == 1 ? OPP(i) : i; }
 
+// PDF i of the state at cell (x, y, z) of a patch (gp: patch base, fp: the
+// cell's flag byte)
 template <typename real>
 __device__ __forceinline__ double read_state(const real *gp, const uint8_t *fp, const real *corr, const Geom &g,
-                                             int rep, int i)
+                                             int rep, int i, int x, int y, int z)
 {
-    if (rep != 2) return (double)gp[rep_slot(rep, i) * g.qs];
-    const int64_t sh = EX(i) + EY(i) * (int64_t)g.px + EZ(i) * g.plane;
-    const uint8_t f = fp[sh];
-    if (i == 0 || f == 0) return (double)gp[i * g.qs + sh];
-    real v = gp[OPP(i) * g.qs];
+    if (rep != 2) return (double)gp[pdf_index(g, rep_slot(rep, i), x, y, z)];
+    const uint8_t f = fp[flag_shift(g, i)];
+    if (i == 0 || f == 0) return (double)gp[pdf_index(g, i, x + EX(i), y + EY(i), z + EZ(i))];
+    real v = gp[pdf_index(g, OPP(i), x, y, z)];
     if (f >= 2) v -= corr[(f - 2) * Q + OPP(i)];
     return (double)v;
 }
@@ -198,9 +200,9 @@ __global__ void import_kernel(const double *canon, int64_t z0, int64_t ncells, i
         const int64_t oz = z0 + r / ny;
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
-        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+        real *gp = grid + (int64_t)lp * g.ps;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) gp[rep_slot(rep, q) * g.qs] = (real)canon[c * Q + q];
+        for (int q = 0; q < Q; ++q) gp[pdf_index(g, rep_slot(rep, q), lx, ly, lz)] = (real)canon[c * Q + q];
     }
 }
 
@@ -218,19 +220,18 @@ __global__ void export_kernel(const real *grid, const uint8_t *flags, int64_t z0
         const int64_t oz = z0 + r / ny;
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
-        const int64_t ci = cell_index(g, lx, ly, lz);
-        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + flag_index(g, lx, ly, lz);
         const bool fluid = fp[0] == 0;
-        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        const real *gp = grid + (int64_t)lp * g.ps;
         if (mode == 0) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+            for (int q = 0; q < Q; ++q) canon[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q, lx, ly, lz) : 0.0;
         } else {
             // Macroscopic export: rho = rho0 + sum f~, u = sum e f~ / rho0.
             double s = 0, jx = 0, jy = 0, jz = 0;
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
-                const double v = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+                const double v = fluid ? read_state(gp, fp, corr, g, rep, q, lx, ly, lz) : 0.0;
                 s += v;
                 jx += EX(q) * v;
                 jy += EY(q) * v;
@@ -298,13 +299,12 @@ __global__ void __launch_bounds__(kMassThreads) mass_kernel(const real *grid, co
         const int64_t oz = r / ny;
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
-        const int64_t ci = cell_index(g, lx, ly, lz);
-        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + flag_index(g, lx, ly, lz);
         if (fp[0] != 0) continue;
-        const real *gp = grid + (int64_t)lp * g.ps + ci;
+        const real *gp = grid + (int64_t)lp * g.ps;
         double cs = 0.0;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) cs += read_state(gp, fp, corr, g, rep, q);
+        for (int q = 0; q < Q; ++q) cs += read_state(gp, fp, corr, g, rep, q, lx, ly, lz);
         s += cs;
     }
     __shared__ double sh[kMassThreads];
@@ -371,12 +371,12 @@ __global__ void noise_kernel(real *grid, uint64_t seed, int64_t NX, int64_t NY, 
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, ox, oy, oz, lp, lx, ly, lz);
         const uint64_t gi = (uint64_t)(((loz + oz) * NY + (loy + oy)) * NX + (lox + ox));
-        real *gp = grid + (int64_t)lp * g.ps + cell_index(g, lx, ly, lz);
+        real *gp = grid + (int64_t)lp * g.ps;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const uint64_t key = gi * 19ull + (uint64_t)q + seed * 0x9E3779B97F4A7C15ull;
             const int64_t k = (int64_t)(splitmix64(key) % 2049ull) - 1024;
-            gp[rep_slot(rep, q) * g.qs] = (real)((double)k * (1.0 / 1048576.0));
+            gp[pdf_index(g, rep_slot(rep, q), lx, ly, lz)] = (real)((double)k * (1.0 / 1048576.0));
         }
     }
 }
@@ -402,11 +402,10 @@ __global__ void gather_kernel(const real *grid, const uint8_t *flags, const int6
     for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         int lp, lx, ly, lz;
         owned_to_patch(g, brick, xyz[3 * c], xyz[3 * c + 1], xyz[3 * c + 2], lp, lx, ly, lz);
-        const int64_t ci = cell_index(g, lx, ly, lz);
-        const uint8_t *fp = flags + (int64_t)lp * g.fs + ci;
+        const uint8_t *fp = flags + (int64_t)lp * g.fs + flag_index(g, lx, ly, lz);
         const bool fluid = fp[0] == 0;
-        const real *gp = grid + (int64_t)lp * g.ps + ci;
-        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q) : 0.0;
+        const real *gp = grid + (int64_t)lp * g.ps;
+        for (int q = 0; q < Q; ++q) out[c * Q + q] = fluid ? read_state(gp, fp, corr, g, rep, q, lx, ly, lz) : 0.0;
     }
 }
 
@@ -439,13 +438,15 @@ __global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *
     const uint8_t *kp = kind + (int64_t)lp * g.fs;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.fs; e += (int64_t)gridDim.x * blockDim.x) {
         if (kp[e] != 1) continue;
+        const int x = (int)(e % g.fpx) - g.fxo;
+        const int64_t r = e / g.fpx;
+        const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
         for (int j = 1; j < Q; ++j) {
-            const int64_t sh = EX(j) + EY(j) * (int64_t)g.px + EZ(j) * g.plane;
-            const uint8_t f = fp[e + sh];
+            const uint8_t f = fp[e + flag_shift(g, j)];
             if (f == 0) continue;
-            real v = gp[(aa ? OPP(j) : j) * g.qs + e];
+            real v = gp[pdf_index(g, aa ? OPP(j) : j, x, y, z)];
             if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
-            gp[(aa ? j : OPP(j)) * g.qs + e + sh] = v;
+            gp[pdf_index(g, aa ? j : OPP(j), x + EX(j), y + EY(j), z + EZ(j))] = v;
         }
     }
 }

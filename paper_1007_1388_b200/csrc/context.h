@@ -23,7 +23,6 @@
 
 namespace lbm {
 
-constexpr int kAlignDefault = 128;  // bytes; interior x = 0 of every row starts on this boundary
 constexpr int kTimingSlots = 64;
 enum Phase { PH_SWEEP = 0, PH_SHELL = 1, PH_INTERIOR = 2, PH_PACK = 3, PH_NCCL = 4, PH_UNPACK = 5, PH_STEP = 6 };
 constexpr int kEvPerSlot = 14;
@@ -84,21 +83,11 @@ struct lbm_ctx {
     Geom g;
     int esize = 8;
     int device = 0;
-    int align = kAlignDefault;
-    // SIMT sweep variants [fp32, fp64] measured best by tools/sweep_tune.py (profiles/r01_sweep_tune_*):
-    // two cells per thread with 2-vector accesses (x2): fp32 4 blocks/SM, fp64 3 blocks/SM (128 threads);
-    // env LBM_SWEEP_VARIANT.
-    int sweep_variant[2] = {12, 13};
-    int aa_variant[2] = {12, 13};  // AA kernels, two cells per thread (tools/sweep_tune.py --layout 1)
-    int direct_variant[2] = {6, 5};  // AA kernels (tools/sweep_tune.py --layout 1): fp32 4 blocks/SM, fp64 2
-    bool use_tma = false;           // TMA-staged sweep (sweep_tma.cu); env LBM_SWEEP_IMPL=tma|simt
+    // x2 sweep occupancy (sweep.cu launch_sweep): 0 = measured best, 1 = the
+    // alternative (env LBM_SWEEP_VARIANT, tools/sweep_tune.py)
+    int sweep_variant = 0;
     int tile_x = SWEEP_BX, tile_y = SWEEP_BY;
     int num_sms = 148;
-    int tma_variant = 0;            // tile shape (sweep_tma.cu TmaShape); env LBM_TMA_SHAPE
-    alignas(64) CUtensorMap tm_pdf[2];   // PDF grids, boxes for the directions with e_x = 0
-    alignas(64) CUtensorMap tm_pdfs[2];  // the same grids, one 64-B chunk wider (e_x != 0)
-    alignas(64) CUtensorMap tm_kind;
-    alignas(64) CUtensorMap tm_flags;
     cudaStream_t stream = nullptr, comm_stream = nullptr;
     // host <-> device transfers (transfer_chunks): two staging buffers and a
     // copy stream, so the DMA of one chunk overlaps the kernel of the next
@@ -110,13 +99,13 @@ struct lbm_ctx {
     void *grid[2] = {nullptr, nullptr};
     int cur = 0;
     uint8_t *flags = nullptr, *kind = nullptr;
+    uint32_t *wmask = nullptr;  // wall-neighbour masks of kind-1 cells (flag layout)
     void *corr = nullptr;
     int *d_origin = nullptr;
     ExSet ex[3];               // indexed by ExKind
-    // Fused exchange (sweep_direct.cu): the sweep stores outgoing PDFs straight
+    // Fused exchange (handshake.cu): the sweep stores outgoing PDFs straight
     // into neighbour ghost layers (local or CUDA-IPC-mapped peer memory).
     bool direct = false;
-    void **d_nbr = nullptr;                 // [nlocal][18][2] neighbour patch bases
     unsigned long long *d_epoch = nullptr;
     unsigned long long *d_inbox = nullptr;  // [nranks] epochs published by the peers
     unsigned long long **d_peer_inbox = nullptr;
@@ -124,14 +113,9 @@ struct lbm_ctx {
     int *d_error = nullptr;
     int npeers_direct = 0;
     std::vector<void *> ipc_mapped;         // peer grids / inboxes opened with cudaIpcOpenMemHandle
-    // Local pull (NEXT-2): face cells read same-GPU neighbour patches directly;
-    // no ghost copies between local patches.
-    bool lpull = false;
-    void **d_lnbr = nullptr;                // [nlocal][18][2]
-    // direct ghost stores by the x2 sweep (same-GPU and, with `direct`, peer patches)
+    // direct ghost stores by the x2 sweeps (same-GPU and, with `direct`, peer patches)
     bool ldirect = false;                   // same-GPU neighbours: no ghost copies
-    bool x2_shells = false;                 // fused exchange: shells swept by the x2 kernel
-    void **d_dnbr = nullptr;                // [nlocal][18][2]
+    void **d_dnbr = nullptr;                // [nlocal][18][2] neighbour patch bases per grid
     std::vector<void *> h_nbr;              // setup_direct's peer-mapped table
     int layout = LBM_LAYOUT_AB;
     int aa_phase = 0;          // AA: 0 swapped (next step PULL), 1 streamed (next step LOCAL)
@@ -243,7 +227,7 @@ inline cudaError_t memset_sync(lbm_ctx *ctx, void *dst, int value, size_t bytes)
 
 extern thread_local std::string g_create_error;  // api.cu: lbm_last_error(NULL)
 
-Geom make_geom(const int n[3], int esize, int align);
+Geom make_geom(const int n[3], int esize);
 
 Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3]);
 
@@ -295,6 +279,11 @@ lbm_status enqueue_step(lbm_ctx *ctx);
 lbm_status ensure_graph(lbm_ctx *ctx);
 
 lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n);
+
+// Fused exchange: wait until every peer has finished storing into this rank's
+// memory for the steps done so far (peers' epoch >= own epoch), then drain
+// both streams.  No-op without peers.
+lbm_status quiesce(lbm_ctx *ctx);
 
 lbm_status transfer_chunks(lbm_ctx *ctx, double *host, bool to_device, int mode, double *rho, double *u);
 

@@ -12,33 +12,7 @@
 
 namespace lbm {
 
-// Direct ghost stores of a cell pair (x0, x0 + 1) -- the pack / copy / unpack of
-// P:331-337 folded into the sweep: a fluid cell on a patch face or edge stores
-// each PDF that travels into the neighbour at d (5 per face, 1 per edge) into
-// that neighbour's ghost cell at the same global position, in the grid the
-// neighbour pulls from next step.  c0 / c1: the cell is fluid and in the box.
-// A ghost column (x = -1, or x = n when sector-aligned) shares its 32-B sector
-// only with row padding, which nothing reads: storing the whole sector (value +
-// zeros) spares L2 the DRAM fill of a partially written sector -- strided
-// 4 / 8-B column stores otherwise cost a read-modify-write each.
-template <typename real>
-__device__ __forceinline__ void st_ghost_sector(real *sector, bool last, real v)
-{
-    if constexpr (sizeof(real) == 4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (last) b.w = v; else a.x = v;
-        reinterpret_cast<float4 *>(sector)[0] = a;
-        reinterpret_cast<float4 *>(sector)[1] = b;
-    } else {
-        double2 a = make_double2(0.0, 0.0), b = a;
-        if (last) b.y = v; else a.x = v;
-        reinterpret_cast<double2 *>(sector)[0] = a;
-        reinterpret_cast<double2 *>(sector)[1] = b;
-    }
-}
-
-// Direct stores toward neighbour kd (compile-time after unrolling) of a cell
-// pair whose cells are on that side (on0 / on1).
+// Neighbour patch kd of `patch` in the destination grid (null: none / copy path).
 template <typename real>
 __device__ __forceinline__ real *direct_ptr(const SweepArgs<real> &a, int patch, int kd)
 {
@@ -46,45 +20,42 @@ __device__ __forceinline__ real *direct_ptr(const SweepArgs<real> &a, int patch,
                                                                       a.dsti));
 }
 
+// Stores toward neighbour KD of the cells of the pair that lie on that side
+// (on0 / on1): each PDF q travelling into the neighbour (5 per face, 1 per edge,
+// P:331-337) goes into the neighbour's ghost cell at the same global position.
+// A y / z face lands in a ghost row / plane of the neighbour's main slices (the
+// pair stays a 2-vector); an x face or an x edge lands in the neighbour's
+// x-ghost column (side 0 of the +x neighbour, side 1 of the -x neighbour).
 template <typename real, int KD, bool OPPSLOT>
-__device__ __forceinline__ void direct_dir_x2(const SweepArgs<real> &a, real *nb, int x0, int y, int z, bool on0,
-                                              bool on1, const real *p0, const real *p1)
+__device__ __forceinline__ void direct_dir_x2(const Geom &g, real *nb, int x0, int y, int z, bool on0, bool on1,
+                                              const real *p0, const real *p1)
 {
     using V2 = typename Vec2<real>::T;
     constexpr int ddx = ndir(KD, 0), ddy = ndir(KD, 1), ddz = ndir(KD, 2);
     if ((!on0 && !on1) || !nb) return;
-    const Geom &g = a.g;
-    const int64_t qs = g.qs;
-    const int n0 = g.n[0];
-    real *gb = nb + cell_index(g, x0 - ddx * n0, y - ddy * g.n[1], z - ddz * g.n[2]);
+    const int ty = y - ddy * g.n[1], tz = z - ddz * g.n[2];
     if constexpr (ddx != 0) {
-        constexpr int SE = 32 / (int)sizeof(real);  // elements per 32-B sector
-        // ghost column x = -1 (ddx > 0) ends a sector; x = n0 (ddx < 0) may start one
-        const bool whole = ddx > 0 ? (g.xo >= SE && g.xo % SE == 0)
-                                   : ((g.xo + n0) % SE == 0 && g.xo + n0 + SE <= g.px);
-        if (whole) {
-            // exactly one cell of the pair lies on the x face (x0 == 0 for ddx < 0;
-            // x0 or x0 + 1 == n0 - 1 for ddx > 0)
-            const real *pv = on0 ? p0 : p1;
-            real *gs = gb + (on0 ? 0 : 1) - (ddx > 0 ? SE - 1 : 0);
+        // exactly one cell of the pair lies on the x face
+        real *gc = nb + ghost_index(g, 0, ddx > 0 ? 0 : 1, ty, tz);
+        const real *pv = on0 ? p0 : p1;
 #pragma unroll
-            for (int q = 1; q < Q; ++q)
-                if (outgoing(q, KD)) st_ghost_sector<real>(gs + (OPPSLOT ? OPP(q) : q) * qs, ddx > 0, pv[q]);
-            return;
-        }
-    }
+        for (int q = 1; q < Q; ++q)
+            if (outgoing(q, KD)) gc[(OPPSLOT ? OPP(q) : q) * g.gq] = pv[q];
+    } else {
+        real *gb = nb + main_index(g, x0, ty, tz);
 #pragma unroll
-    for (int q = 1; q < Q; ++q) {
-        if (!outgoing(q, KD)) continue;
-        const int64_t sl = (OPPSLOT ? OPP(q) : q) * qs;
-        if (ddx == 0 && on0 && on1) {  // same x as the pair: aligned 2-vector
-            V2 w;
-            w.x = p0[q];
-            w.y = p1[q];
-            *reinterpret_cast<V2 *>(gb + sl) = w;
-        } else {
-            if (on0) gb[sl] = p0[q];
-            if (on1) gb[sl + 1] = p1[q];
+        for (int q = 1; q < Q; ++q) {
+            if (!outgoing(q, KD)) continue;
+            const int64_t sl = (OPPSLOT ? OPP(q) : q) * g.qs;
+            if (on0 && on1) {  // same x as the pair: aligned 2-vector
+                V2 w;
+                w.x = p0[q];
+                w.y = p1[q];
+                *reinterpret_cast<V2 *>(gb + sl) = w;
+            } else {
+                if (on0) gb[sl] = p0[q];
+                if (on1) gb[sl + 1] = p1[q];
+            }
         }
     }
 }
@@ -104,7 +75,7 @@ __device__ __forceinline__ void direct_dir_x2_on(const SweepArgs<real> &a, int p
         on0 = on0 && x0 == n0 - 1;
         on1 = on1 && x0 + 1 == n0 - 1;
     }
-    if (on0 || on1) direct_dir_x2<real, KD, OPPSLOT>(a, direct_ptr(a, patch, KD), x0, y, z, on0, on1, p0, p1);
+    if (on0 || on1) direct_dir_x2<real, KD, OPPSLOT>(a.g, direct_ptr(a, patch, KD), x0, y, z, on0, on1, p0, p1);
 }
 
 template <typename real, bool OPPSLOT, int... KD>
@@ -136,11 +107,10 @@ __device__ __forceinline__ void direct_stores_x2(const SweepArgs<real> &a, int p
     if (!yzf) {
         const bool hi0 = c0 && x0 == n0 - 1, hi1 = c1 && x0 + 1 == n0 - 1;
         if (x0 == 0) {
-            direct_dir_x2<real, 8, OPPSLOT>(a, nb_x, x0, y, z, c0, false, p0, p1);
-            if (hi0 || hi1)
-                direct_dir_x2<real, 9, OPPSLOT>(a, direct_ptr(a, patch, 9), x0, y, z, hi0, hi1, p0, p1);
+            direct_dir_x2<real, 8, OPPSLOT>(g, nb_x, x0, y, z, c0, false, p0, p1);
+            if (hi0 || hi1) direct_dir_x2<real, 9, OPPSLOT>(g, direct_ptr(a, patch, 9), x0, y, z, hi0, hi1, p0, p1);
         } else {
-            direct_dir_x2<real, 9, OPPSLOT>(a, nb_x, x0, y, z, hi0, hi1, p0, p1);
+            direct_dir_x2<real, 9, OPPSLOT>(g, nb_x, x0, y, z, hi0, hi1, p0, p1);
         }
         return;
     }

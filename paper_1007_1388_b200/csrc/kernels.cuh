@@ -1,4 +1,4 @@
-// kernels.cuh -- launch wrappers of the sm_100a kernels (sweep.cu, sweep_aa.cu, aux_kernels.cu, sweep_direct.cu, sweep_tma.cu).
+// kernels.cuh -- launch wrappers of the sm_100a kernels (sweep.cu, sweep_aa.cu, aux_kernels.cu, handshake.cu).
 #pragma once
 
 #include <cuda.h>
@@ -18,23 +18,19 @@ template <typename real>
 struct SweepArgs {
     const real *src;
     real *dst;
-    const uint8_t *flags;   // [patch][fs] raw cell flags incl. ghost layer
+    const uint8_t *flags;   // [patch][fs] raw cell flags incl. ghost layer (flag layout)
     const uint8_t *kind;    // [patch][fs] 0 fluid (all neighbours fluid), 1 fluid next to a wall, 2 non-fluid
+    const uint32_t *wmask;  // [patch][fs] kind-1 cells: bit j set if x + e_j is non-fluid
     const real *corr;       // [nvel][19]: 6 w_i rho0 (e_i . u_w[k]) rounded to real
     Geom g;
     real omega;
     const Box *boxes;       // device
     const int64_t *tile_prefix; // device, nboxes + 1
     int nboxes;
-    // Local pull (NEXT-2): [nlocal][18][2] base of the same-GPU neighbour patch in
-    // grid i (null: no local neighbour); face cells pull from it directly instead
-    // of from a ghost copy.  lnbr == nullptr disables it.
-    const real *const *lnbr = nullptr;
-    int srci = 0;
-    // Direct ghost stores (x2 sweep): [nlocal][18][2] base of the neighbour patch
-    // (same GPU, or peer-mapped) in grid i, null where the copy path serves it.
-    // Face / edge cells store their outgoing PDFs into that patch's ghost cell
-    // of grid dsti.  dnbr == nullptr disables it.
+    // Direct ghost stores: [nlocal][18][2] base of the neighbour patch (same GPU,
+    // or peer-mapped) in grid i, null where the copy path serves it.  Face / edge
+    // cells store their outgoing PDFs into that patch's ghost cells of grid dsti.
+    // dnbr == nullptr disables them.
     real *const *dnbr = nullptr;
     int dsti = 0;
 };
@@ -56,41 +52,18 @@ __host__ __device__ constexpr bool outgoing(int q, int k)
            (ndir(k, 2) == 0 || EZf(q) == ndir(k, 2));
 }
 
-// variant 0..7 = 2 * m + stcs: min blocks per SM = m + 1, stcs = evict-first stores,
-// one cell per thread; variants 8..11: two cells per thread along z (tiles span
-// 2 planes), min blocks 2 / 3, stcs 0 / 1.
+// Two-grid sweep (sweep.cu): two cells per thread along x, 2-vector accesses;
+// variant 0: default occupancy (fp64 3, fp32 4 blocks of 128 threads per SM),
+// 1: the alternative (fp64 2, fp32 5).
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s);
+constexpr int kSweepVariants = 2;
 
-// Sweep fused with the ghost exchange (sweep_direct.cu).
-template <typename real>
-struct DirectArgs {
-    real *const *nbr;  // [nlocal][18][2]: remote neighbour patch base in (peer-mapped) grid i, or null
-    int dsti;          // destination grid index (0 / 1)
-};
-template <typename real>
-cudaError_t launch_sweep_direct(const SweepArgs<real> &a, const DirectArgs<real> &dx, int64_t total_tiles,
-                                int variant, cudaStream_t s);
+// Fused-exchange handshake (handshake.cu).
 cudaError_t launch_wait_peers(const unsigned long long *inbox, const int *peer_rank, int npeers,
                               const unsigned long long *epoch, int *error, cudaStream_t s);
 cudaError_t launch_signal_peers(unsigned long long *epoch, unsigned long long *const *peer_inbox, int npeers,
                                 cudaStream_t s);
-// variants 12..15: two cells per thread along x, 2-vector accesses,
-// min blocks 4 / 5 of 128 threads, stcs 0 / 1.
-constexpr int kSweepVariants = 16;
-__host__ __device__ constexpr int sweep_cells_z(int variant) { return (variant >= 8 && variant < 12) ? 2 : 1; }
-
-// TMA-staged persistent sweep (sweep_tma.cu); variant selects the tile shape.
-template <typename real>
-void tma_tile_shape(int variant, int *tx, int *ty);
-template <typename real>
-cudaError_t make_tma_maps(const void *grid, const uint8_t *kind, const uint8_t *flags, int nlocal, const Geom &g,
-                          int variant, CUtensorMap *pdf_map, CUtensorMap *pdfs_map, CUtensorMap *kind_map,
-                          CUtensorMap *flag_map);
-template <typename real>
-cudaError_t launch_sweep_tma(const CUtensorMap &pdf_map, const CUtensorMap &pdfs_map, const CUtensorMap &kind_map,
-                             const CUtensorMap &flag_map, const SweepArgs<real> &a, int64_t total_tiles, int num_sms,
-                             int variant, cudaStream_t s);
 
 // Total mass: sum of delta rho over the owned fluid cells into *out (fp64,
 // deterministic; partial: kMassBlocks doubles of scratch).
@@ -111,15 +84,17 @@ template <typename real>
 cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
                            const Geom &g, int aa, cudaStream_t s);
 
-// AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL.
+// AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL;
+// variant as launch_sweep.
 template <typename real>
 cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool pull, int variant, cudaStream_t s);
 
 // Build per-patch flags (incl. ghosts, periodic wrap) from the global flag
-// array (device copy, (nz+2)(ny+2)(nx+2)), then the per-cell kind.
+// array (device copy, (nz+2)(ny+2)(nx+2)), then the per-cell kind and the
+// wall-neighbour masks of kind-1 cells.
 cudaError_t launch_build_flags(const uint8_t *global, const int64_t domain[3], const int periodic[3],
                                const int *patch_origin /*3 per local patch*/, int nlocal, const Geom &g,
-                               uint8_t *flags, uint8_t *kind, cudaStream_t s);
+                               uint8_t *flags, uint8_t *kind, uint32_t *wmask, cudaStream_t s);
 
 // Import / export between the canonical double [z][y][x][19] layout of a
 // range of owned z-planes and the patch grids.  rep: 0 two-grid, 1 AA

@@ -41,19 +41,60 @@ constexpr int NDIR = 18;
 struct Dir3 { int d[3]; };
 
 // Patch geometry shared by every patch of a ctx (all patches have one size).
-// Element index of cell (x, y, z), -1 <= x,y,z <= n, inside one q-slice:
-//   ((z + 1) * py + (y + 1)) * px + (x + xo)
-// px is padded so that x = 0 starts on an `align`-byte boundary; q-slices and
-// patches are laid out back to back: [patch][q][z][y][x].
+// PDF storage of one patch (elements, back to back; patches back to back):
+//   main q-slices  [q][z = -1..n2][y = -1..n1][x = 0..n0-1]: rows of exactly
+//                  n0 cells (px = n0 rounded up to a 32-B sector, = n0 for
+//                  every BASELINE size) with the y / z ghost rows and planes;
+//   x-ghost columns [q][side][z = -1..n2][y = -1..n1] (side 0: x = -1,
+//                  side 1: x = n0), y = 0 on a sector boundary.
+// Unpadded rows stream better than rows padded for an in-row x ghost (the
+// access pattern's own ceiling drops 5-7 % at 256^3 and 17 % for 64^3 patches,
+// profiles/r01_stream_ceiling_*compact.log), and a patch's x faces become
+// y-contiguous runs for the exchange.
+// Flags and cell kinds (uint8) keep an in-row x ghost: [z][y][x = -1..n0],
+// row pitch fpx, x = 0 at offset fxo (even, so a cell pair is one uchar2).
 struct Geom {
     int n[3];        // patch interior size
-    int px, py;      // row pitch (elements), rows per plane (n[1] + 2)
-    int xo;          // element offset of interior x = 0 in a row
+    int px, py;      // PDF row pitch (elements), rows per plane (n1 + 2)
     int64_t plane;   // px * py
-    int64_t qs;      // elements per q-slice = plane * (n[2] + 2)
-    int64_t ps;      // elements per patch = 19 * qs
-    int64_t fs;      // flag bytes per patch = qs
+    int64_t qs;      // elements per main q-slice (plane * (n2 + 2), rounded up to 32)
+    int gy, gyo;     // x-ghost column: pitch per z plane, offset of y = 0
+    int64_t gside;   // gy * (n2 + 2): one x-ghost column (one side, one q)
+    int64_t gq;      // 2 * gside: both sides of one q
+    int64_t gbase;   // Q * qs: start of the x-ghost columns in a patch
+    int64_t ps;      // elements per patch (main + ghosts, rounded up to 32)
+    int fpx, fxo;    // flag row pitch, offset of x = 0 in a flag row
+    int64_t fplane;  // fpx * py
+    int64_t fs;      // flag bytes per patch = fplane * (n2 + 2)
 };
+
+#ifndef __CUDACC__
+#define LBM_HD inline
+#else
+#define LBM_HD __host__ __device__ __forceinline__
+#endif
+// element of interior cell (x, y, z), 0 <= x < n0, -1 <= y <= n1, -1 <= z <= n2, in a main q-slice
+LBM_HD int64_t main_index(const Geom &g, int x, int y, int z)
+{
+    return ((int64_t)(z + 1) * g.py + (y + 1)) * (int64_t)g.px + x;
+}
+// element of x-ghost cell (side 0: x = -1, 1: x = n0) of direction q, relative to the patch base
+LBM_HD int64_t ghost_index(const Geom &g, int q, int side, int y, int z)
+{
+    return g.gbase + (int64_t)q * g.gq + side * g.gside + (int64_t)(z + 1) * g.gy + (y + g.gyo);
+}
+// element of PDF q of any cell -1 <= x, y, z <= n, relative to the patch base
+LBM_HD int64_t pdf_index(const Geom &g, int q, int x, int y, int z)
+{
+    if (x < 0) return ghost_index(g, q, 0, y, z);
+    if (x >= g.n[0]) return ghost_index(g, q, 1, y, z);
+    return (int64_t)q * g.qs + main_index(g, x, y, z);
+}
+// flag / kind byte of cell (x, y, z), relative to the patch's flag base
+LBM_HD int64_t flag_index(const Geom &g, int x, int y, int z)
+{
+    return ((int64_t)(z + 1) * g.py + (y + 1)) * (int64_t)g.fpx + (x + g.fxo);
+}
 
 // Sweep box: cells [lo, lo + n) of local patch `patch`.
 struct Box {

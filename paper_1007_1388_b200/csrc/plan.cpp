@@ -79,8 +79,10 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
     if (!(cfg.omega > 0.0 && cfg.omega < 2.0)) return "omega must satisfy 0 < omega < 2";
     if (cfg.precision != LBM_FP32 && cfg.precision != LBM_FP64) return "precision must be LBM_FP32 (4) or LBM_FP64 (8)";
     if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks) return "need 0 <= rank < nranks";
-    if (cfg.exchange_mode != LBM_EXCHANGE_AUTO && cfg.exchange_mode != LBM_EXCHANGE_FORCE_BUFFERS)
+    if (cfg.exchange_mode != LBM_EXCHANGE_AUTO && cfg.exchange_mode != LBM_EXCHANGE_FORCE_BUFFERS &&
+        cfg.exchange_mode != LBM_EXCHANGE_SELF_PEER)
         return "unknown exchange_mode";
+    if (cfg.exchange_mode == LBM_EXCHANGE_SELF_PEER && cfg.nranks != 1) return "exchange_mode SELF_PEER needs nranks == 1";
     if (cfg.layout != LBM_LAYOUT_AB && cfg.layout != LBM_LAYOUT_AA) return "unknown layout";
     int pg[3] = {cfg.proc_grid[0], cfg.proc_grid[1], cfg.proc_grid[2]};
     if (pg[0] == 0 && pg[1] == 0 && pg[2] == 0) {
@@ -110,7 +112,9 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
     dec.coord[0] = cfg.rank % pg[0];
     dec.coord[1] = (cfg.rank / pg[0]) % pg[1];
     dec.coord[2] = cfg.rank / (pg[0] * pg[1]);
-    dec.force_buffers = cfg.exchange_mode == LBM_EXCHANGE_FORCE_BUFFERS;
+    // FORCE_BUFFERS and SELF_PEER: same-rank neighbours are planned as remote
+    // segments (peer = this rank)
+    dec.force_buffers = cfg.exchange_mode != LBM_EXCHANGE_AUTO;
     dec.nlocal = dec.brick[0] * dec.brick[1] * dec.brick[2];
     for (int a = 0; a < 3; ++a) {
         dec.owned_lo[a] = (int64_t)dec.coord[a] * dec.brick[a] * dec.patch[a];

@@ -12,20 +12,26 @@
 
 namespace lbm {
 
-Geom make_geom(const int n[3], int esize, int align)
+Geom make_geom(const int n[3], int esize)
 {
     Geom g;
     for (int a = 0; a < 3; ++a) g.n[a] = n[a];
-    const int ae = align / esize;             // elements per alignment unit
-    g.xo = ae;                                // x = -1 sits right before the aligned x = 0
-    // columns up to x = n + 1 must exist: the two-cells-per-thread kernels read
-    // the phantom partner x0 + 1 = n of an odd row and its pull neighbour n + 1
-    g.px = ((g.xo + n[0] + 2 + ae - 1) / ae) * ae;
+    const int se = 32 / esize;                  // elements per 32-B sector
+    auto up = [](int64_t v, int64_t m) { return (v + m - 1) / m * m; };
+    g.px = (int)up(n[0], se);                   // unpadded rows (= n0 when n0 fills whole sectors)
     g.py = n[1] + 2;
     g.plane = (int64_t)g.px * g.py;
-    g.qs = g.plane * (n[2] + 2);
-    g.ps = (int64_t)Q * g.qs;
-    g.fs = g.qs;
+    g.qs = up(g.plane * (n[2] + 2), 32);
+    g.gyo = se;                                 // y = 0 on a sector boundary, y = -1 just before it
+    g.gy = (int)up(g.gyo + n[1] + 1, se);
+    g.gside = (int64_t)g.gy * (n[2] + 2);
+    g.gq = 2 * g.gside;
+    g.gbase = (int64_t)Q * g.qs;
+    g.ps = up(g.gbase + (int64_t)Q * g.gq, 32);
+    g.fxo = 4;                                  // even: a cell pair's kinds are one uchar2
+    g.fpx = (int)up(g.fxo + n[0] + 1, 4);
+    g.fplane = (int64_t)g.fpx * g.py;
+    g.fs = g.fplane * (n[2] + 2);
     return g;
 }
 
@@ -47,12 +53,7 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
     std::vector<int64_t> prefix(boxes.size() + 1, 0);
     for (size_t i = 0; i < boxes.size(); ++i) {
         const Box &b = boxes[i];
-        const int zc = (ctx->use_tma || ctx->layout == LBM_LAYOUT_AA)
-                           ? 1
-                           : sweep_cells_z(ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]);
-        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0)
-                        ? (int64_t)b.tiles_x * b.tiles_y * ((b.n[2] + zc - 1) / zc)
-                        : 0;
+        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0) ? (int64_t)b.tiles_x * b.tiles_y * b.n[2] : 0;
         prefix[i + 1] = prefix[i] + t;
     }
     out.n = (int)boxes.size();
@@ -302,9 +303,8 @@ lbm_status build_boxes(lbm_ctx *ctx, bool whole_x)
             lo[a] = th[2 * a];
             hi[a] = n[a] - th[2 * a + 1];
         }
-        // Every tile must start on a 16-cell boundary in x (16-B aligned TMA
-        // starts for the PDF, kind and flag maps, see sweep_tma.cu): round the
-        // high-x shell start down.
+        // Every box starts on an even x (cell pairs) and a 16-cell boundary in x
+        // (whole 64-B chunks for fp32): round the high-x shell start down.
         const int xa = 16;
         hi[0] = std::max(lo[0], hi[0] / xa * xa);
         // z slabs (full xy), then y slabs (full x, inner z), then x slabs (inner y, z)
@@ -351,7 +351,10 @@ lbm_status setup_exchange(lbm_ctx *ctx)
     if ((st = dev_alloc(ctx, &ctx->recvbuf, (size_t)ro * ctx->esize))) return st;
 
     if ((st = build_boxes(ctx, false))) return st;
-    ctx->use_overlap = ctx->cfg.overlap && ctx->has_nccl;
+    // Shells first, transport overlapped with the interiors, whenever anything
+    // goes through the buffers -- also a one-GPU FORCE_BUFFERS run, whose
+    // self-peer messages travel through a one-rank NCCL communicator.
+    ctx->use_overlap = ctx->cfg.overlap && ctx->has_remote;
     return LBM_OK;
 }
 
@@ -365,7 +368,7 @@ lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u,
     cudaError_t e = upload(ctx, dflags, flags, total);
     if (e == cudaSuccess)
         e = launch_build_flags(dflags, ctx->dec.domain, ctx->dec.periodic, ctx->d_origin, ctx->dec.nlocal, ctx->g,
-                               ctx->flags, ctx->kind, ctx->stream);
+                               ctx->flags, ctx->kind, ctx->wmask, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     cudaFree(dflags);
     ctx->device_bytes -= (int64_t)total;
@@ -444,20 +447,24 @@ void destroy_ctx(lbm_ctx *ctx)
 {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    // Fused exchange: peers may still be storing into this rank's grid and inbox
+    // (their last step); wait for them before freeing (best effort: a poisoned
+    // context skips it, a dead peer times out).
+    if (!ctx->poisoned) quiesce(ctx);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
     for (int i = 0; i < 2; ++i)
         if (ctx->graph[i]) cudaGraphExecDestroy(ctx->graph[i]);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     for (void *p : ctx->ipc_mapped) cudaIpcCloseMemHandle(p);
-    for (void *p : {(void *)ctx->d_mass, (void *)ctx->d_lnbr, (void *)ctx->d_dnbr, (void *)ctx->d_nbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
+    for (void *p : {(void *)ctx->d_mass, (void *)ctx->d_dnbr, (void *)ctx->d_epoch, (void *)ctx->d_inbox,
                     (void *)ctx->d_peer_inbox, (void *)ctx->d_peer_rank, (void *)ctx->d_error})
         if (p) cudaFree(p);
     for (ExSet &X : ctx->ex)
         for (void *p : {(void *)X.pack_all.segs, (void *)X.pack_remote.segs, (void *)X.local_copy.segs,
                         (void *)X.unpack.segs})
             if (p) cudaFree(p);
-    void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->corr, ctx->d_origin, ctx->sendbuf,
+    void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
                     ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
                     ctx->box_interior.boxes, ctx->box_interior.prefix};
@@ -492,13 +499,22 @@ lbm_status setup_direct(lbm_ctx *ctx)
     CK(memset_sync(ctx, ctx->d_epoch, 0, sizeof(unsigned long long)));
     CK(memset_sync(ctx, ctx->d_inbox, 0, (size_t)R * sizeof(unsigned long long)));
     CK(memset_sync(ctx, ctx->d_error, 0, sizeof(int)));
-    // Remote peers of the exchange plan.
+    // Remote peers of the exchange plan.  exchange_mode SELF_PEER (one GPU): this
+    // rank is its own peer -- every neighbour patch is reached through the peer
+    // table and the epoch handshake exactly as across GPUs, with its own grid and
+    // inbox in place of IPC-mapped ones.
+    const bool self = ctx->cfg.exchange_mode == LBM_EXCHANGE_SELF_PEER;
     std::vector<int> peers;
     for (const Peer &p : ctx->ex[EX_AB].peers)
-        if (p.rank != me) peers.push_back(p.rank);
+        if (p.rank != me || self) peers.push_back(p.rank);
     if (peers.empty()) return LBM_OK;  // nothing crosses a GPU boundary: copy path
     std::vector<void *> peer_grid((size_t)R * 2, nullptr), peer_inbox((size_t)R, nullptr);
-    {
+    if (self) {
+        const bool aa = ctx->layout == LBM_LAYOUT_AA;
+        peer_grid[(size_t)2 * me] = ctx->grid[0];
+        peer_grid[(size_t)2 * me + 1] = ctx->grid[aa ? 0 : 1];
+        peer_inbox[me] = ctx->d_inbox;
+    } else {
         // all-gather {grid0, grid1, inbox} IPC handles
         const size_t hb = sizeof(cudaIpcMemHandle_t);
         std::vector<cudaIpcMemHandle_t> mine(3);
@@ -556,7 +572,7 @@ lbm_status setup_direct(lbm_ctx *ctx)
             const int nbp = neighbour(dec, gpatch, kDirs[k].d);
             if (nbp < 0) continue;
             const int r = dec.owner(nbp);
-            if (r == me) continue;  // same-GPU neighbours: ghost copy after the sweep
+            if (r == me && !self) continue;  // same-GPU neighbours: direct stores / ghost copies
             const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
             for (int i = 0; i < 2; ++i) {
                 char *base = (char *)peer_grid[(size_t)2 * r + i];
@@ -565,8 +581,6 @@ lbm_status setup_direct(lbm_ctx *ctx)
         }
     }
     ctx->h_nbr = nbr;
-    if ((st = dev_alloc(ctx, &ctx->d_nbr, nbr.size() * sizeof(void *)))) return st;
-    CK(upload(ctx, ctx->d_nbr, nbr.data(), nbr.size() * sizeof(void *)));
     std::vector<unsigned long long *> pin;
     std::vector<int> prank;
     for (int r : peers) {
@@ -611,36 +625,9 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     ctx->dec = dec;
     ctx->esize = cfg->precision;
     ctx->layout = cfg->layout;
-    if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {
-        int v = std::atoi(a);
-        if (v >= 0 && v < kSweepVariants) {
-            ctx->sweep_variant[0] = ctx->sweep_variant[1] = v;
-        }
-        if ((v >= 0 && v < 8) || v >= 12) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
-        if (v >= 4 && v < 8) ctx->direct_variant[0] = ctx->direct_variant[1] = v;
-    }
-    if (const char *a = std::getenv("LBM_AA_VARIANT")) {  // AA kernels alone (12..15, sweep_aa.cu launch_aa_x2)
-        int v = std::atoi(a);
-        if ((v >= 0 && v < 8) || (v >= 12 && v < kSweepVariants)) ctx->aa_variant[0] = ctx->aa_variant[1] = v;
-    }
-    if (const char *a = std::getenv("LBM_SWEEP_IMPL")) {
-        if (std::string(a) == "simt") ctx->use_tma = false;
-        if (std::string(a) == "tma") ctx->use_tma = true;
-    }
-    if (ctx->layout == LBM_LAYOUT_AA) ctx->use_tma = false;  // the AA kernels are SIMT
-    if (const char *a = std::getenv("LBM_TMA_SHAPE")) {
-        int v = std::atoi(a);
-        if (v >= 0 && v <= 2) ctx->tma_variant = v;
-    }
-    if (ctx->use_tma) {
-        if (ctx->esize == 8)
-            tma_tile_shape<double>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
-        else
-            tma_tile_shape<float>(ctx->tma_variant, &ctx->tile_x, &ctx->tile_y);
-    }
-    if (const char *a = std::getenv("LBM_ALIGN_BYTES")) {
-        int v = std::atoi(a);
-        if (v >= ctx->esize && v <= 1024 && (v & (v - 1)) == 0) ctx->align = v;
+    if (const char *a = std::getenv("LBM_SWEEP_VARIANT")) {  // occupancy alternative (tools/sweep_tune.py)
+        const int v = std::atoi(a);
+        if (v >= 0 && v < kSweepVariants) ctx->sweep_variant = v;
     }
     auto bail = [&](lbm_status st) {
         g_create_error = ctx->err.empty() ? "create failed" : ctx->err;
@@ -672,7 +659,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             return bail(LBM_ERR_CUDA);
         }
     }
-    ctx->g = make_geom(dec.patch, ctx->esize, ctx->align);
+    ctx->g = make_geom(dec.patch, ctx->esize);
     lbm_status st;
     // Streams and events
     if (cfg->stream) {
@@ -721,6 +708,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
     }
     if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->wmask, flag_bytes * sizeof(uint32_t)))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->corr, (size_t)LBM_MAX_WALL_VELOCITIES * Q * ctx->esize))) return bail(st);
     {
         std::vector<int> origin(3 * dec.nlocal);
@@ -739,26 +727,18 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
             ctx->num_sms = sms;
     }
-    if (ctx->use_tma) {
-        for (int i = 0; i < 2; ++i) {
-            cudaError_t e = ctx->esize == 8
-                                ? make_tma_maps<double>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
-                                                        ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_pdfs[i],
-                                                        &ctx->tm_kind, &ctx->tm_flags)
-                                : make_tma_maps<float>(ctx->grid[i], ctx->kind, ctx->flags, dec.nlocal, ctx->g,
-                                                       ctx->tma_variant, &ctx->tm_pdf[i], &ctx->tm_pdfs[i],
-                                                       &ctx->tm_kind, &ctx->tm_flags);
-            if (e != cudaSuccess) {
-                ctx->err = "cuTensorMapEncodeTiled failed for the PDF / kind arrays";
-                return bail(LBM_ERR_CUDA);
-            }
-        }
-    }
     if ((st = setup_exchange(ctx))) return bail(st);
-    // NCCL communicator (bootstrap id broadcast by the caller, e.g. torch.distributed)
-    if (cfg->nranks > 1) {
+    // NCCL communicator (bootstrap id broadcast by the caller, e.g. torch.distributed).
+    // One GPU with FORCE_BUFFERS: a one-rank communicator, so the self-peer
+    // messages take the grouped ncclSend / ncclRecv path of P:287-313.
+    if (cfg->nranks > 1 || (ctx->has_remote && cfg->exchange_mode == LBM_EXCHANGE_FORCE_BUFFERS)) {
         ncclUniqueId id;
-        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        if (cfg->nranks > 1) {
+            std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        } else if (ncclGetUniqueId(&id) != ncclSuccess) {
+            ctx->err = "ncclGetUniqueId failed";
+            return bail(LBM_ERR_NCCL);
+        }
         ncclResult_t r = ncclCommInitRank(&ctx->nccl, cfg->nranks, id, cfg->rank);
         if (r != ncclSuccess) {
             ctx->nccl = nullptr;
@@ -766,65 +746,26 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
             return bail(LBM_ERR_NCCL);
         }
     }
-    // The x2 sweeps (two-grid: sweep.cu, AA: sweep_aa.cu) can store the outgoing
-    // PDFs of face cells straight into neighbour patches (direct ghost stores).
+    // Fused exchange across GPUs (and with exchange_mode SELF_PEER on one GPU)
+    // unless the NCCL path is requested (exchange_mode FORCE_BUFFERS, or env
+    // LBM_EXCHANGE=nccl).
     const bool aa = ctx->layout == LBM_LAYOUT_AA;
-    const bool x2 = !ctx->use_tma && cfg->exchange_mode == LBM_EXCHANGE_AUTO &&
-                    (aa ? ctx->aa_variant[ctx->esize == 8 ? 1 : 0] : ctx->sweep_variant[ctx->esize == 8 ? 1 : 0]) >= 12;
-    const char *e_shell = std::getenv("LBM_SHELL_KERNEL");
-    const bool onecell = e_shell && std::string(e_shell) == "onecell";
     {
-        // Fused exchange across GPUs unless the NCCL path is requested (exchange_mode
-        // FORCE_BUFFERS, or env LBM_EXCHANGE=nccl); the AA layout needs the x2 kernels
-        // (its shells have no one-cell fused kernel).
         const char *ev = std::getenv("LBM_EXCHANGE");
-        const bool want = cfg->exchange_mode == LBM_EXCHANGE_AUTO && !(ev && std::string(ev) == "nccl") &&
-                          (!aa || (x2 && !onecell));
+        const bool want = cfg->exchange_mode != LBM_EXCHANGE_FORCE_BUFFERS && !(ev && std::string(ev) == "nccl");
         if (want && (st = setup_direct(ctx))) return bail(st);
     }
     {
-        // Local pull for the SIMT two-grid sweep when same-GPU neighbours exist.
-        // Opt-in: measured slower than the ghost copies on B200.
-        const char *ev = std::getenv("LBM_LOCAL_PULL");
-        const int v = ctx->sweep_variant[ctx->esize == 8 ? 1 : 0];
-        const bool want = ctx->layout == LBM_LAYOUT_AB && !ctx->use_tma && !ctx->direct &&
-                          cfg->exchange_mode == LBM_EXCHANGE_AUTO && v >= 4 && v < 8 &&
-                          (ev && std::string(ev) == "1") && !ctx->ex[EX_AB].segs.local.empty();
-        if (want) {
-            std::vector<void *> tab((size_t)dec.nlocal * NDIR * 2, nullptr);
-            for (int l = 0; l < dec.nlocal; ++l) {
-                const int gp = dec.local_to_global(l);
-                for (int k = 0; k < NDIR; ++k) {
-                    const int nbp = neighbour(dec, gp, kDirs[k].d);
-                    if (nbp < 0 || dec.owner(nbp) != dec.rank) continue;
-                    const int64_t off = (int64_t)dec.local_index_on_owner(nbp) * ctx->g.ps * ctx->esize;
-                    for (int i = 0; i < 2; ++i) tab[((size_t)l * NDIR + k) * 2 + i] = (char *)ctx->grid[i] + off;
-                }
-            }
-            if ((st = dev_alloc(ctx, &ctx->d_lnbr, tab.size() * sizeof(void *)))) return bail(st);
-            if (upload(ctx, ctx->d_lnbr, tab.data(), tab.size() * sizeof(void *)) !=
-                cudaSuccess)
-                return bail(LBM_ERR_CUDA);
-            ctx->lpull = true;
-        }
-    }
-    {
-        // Direct ghost stores by the two-grid x2 sweep: face / edge cells write
-        // their outgoing PDFs straight into the neighbour patches' ghost layers.
+        // Direct ghost stores by the x2 sweeps: face / edge cells write their
+        // outgoing PDFs straight into the neighbour patches' ghost layers.
         // (1) same-GPU neighbours, replacing the ghost copies after the sweep
         //     (default; LBM_LOCAL_DIRECT=0 keeps the copies);
-        // (2) with the fused exchange, the shells facing other GPUs are swept by
-        //     the same kernel through the peer-mapped table instead of the
-        //     one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell keeps it).
-        // AA default: only for small patches -- the AA direct kernels spill, which
-        // costs 3.8 % of the sweep at 384^3 (more than the ghost copies), while at
-        // 64^3 the copies cost more; LBM_LOCAL_DIRECT=1 / 0 forces it.
+        // (2) with the fused exchange, the shells facing other GPUs store
+        //     through the peer-mapped table.
         const char *ev = std::getenv("LBM_LOCAL_DIRECT");
-        const int pmin = std::min(ctx->g.n[0], std::min(ctx->g.n[1], ctx->g.n[2]));
-        const bool dflt = !aa || pmin <= 128;
-        const bool on = ev ? std::string(ev) != "0" : dflt;
-        const bool want_local = x2 && !ctx->lpull && on && !ctx->ex[EX_AB].segs.local.empty();
-        const bool want_shell = x2 && ctx->direct && !onecell;
+        const bool on = ev ? std::string(ev) != "0" : true;
+        const bool want_local = on && cfg->exchange_mode == LBM_EXCHANGE_AUTO && !ctx->ex[EX_AB].segs.local.empty();
+        const bool want_shell = ctx->direct;
         if (want_local || want_shell) {
             std::vector<void *> tab = ctx->direct ? ctx->h_nbr : std::vector<void *>((size_t)dec.nlocal * NDIR * 2, nullptr);
             for (int l = 0; l < dec.nlocal && want_local; ++l) {
@@ -838,19 +779,13 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
                 }
             }
             if ((st = dev_alloc(ctx, &ctx->d_dnbr, tab.size() * sizeof(void *)))) return bail(st);
-            if (upload(ctx, ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *)) !=
-                cudaSuccess)
+            if (upload(ctx, ctx->d_dnbr, tab.data(), tab.size() * sizeof(void *)) != cudaSuccess)
                 return bail(LBM_ERR_CUDA);
             ctx->ldirect = want_local;
-            ctx->x2_shells = want_shell;
         }
     }
-    if (ctx->direct) {
-        // fused exchange: patches with a remote x side are swept whole (build_boxes);
-        // LBM_XSHELL=slab keeps the SWEEP_BX-wide x slabs
-        const char *ev = std::getenv("LBM_XSHELL");
-        if (!(ev && std::string(ev) == "slab") && (st = build_boxes(ctx, true))) return bail(st);
-    }
+    // fused exchange: patches with a remote x side are swept whole (build_boxes)
+    if (ctx->direct && (st = build_boxes(ctx, true))) return bail(st);
     // Default geometry: closed no-slip box at rest (f~ = 0).
     {
         const int64_t nx = dec.domain[0], ny = dec.domain[1], nz = dec.domain[2];

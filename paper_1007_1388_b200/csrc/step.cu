@@ -26,14 +26,13 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     }
     a.flags = ctx->flags;
     a.kind = ctx->kind;
+    a.wmask = ctx->wmask;
     a.corr = (const real *)ctx->corr;
     a.g = ctx->g;
     a.omega = (real)ctx->cfg.omega;
     a.boxes = b.boxes;
     a.tile_prefix = b.prefix;
     a.nboxes = b.n;
-    a.lnbr = ctx->lpull ? (const real *const *)ctx->d_lnbr : nullptr;
-    a.srci = ctx->cur;
     a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
     a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
     return a;
@@ -46,21 +45,13 @@ lbm_status launch_sweep_set(lbm_ctx *ctx, const DevBoxes &b, cudaStream_t s)
     if (ctx->layout == LBM_LAYOUT_AA) {
         const bool pull = ctx->aa_phase == 0;
         if (ctx->esize == 8)
-            e = launch_sweep_aa<double>(sweep_args<double>(ctx, b), b.tiles, pull, ctx->aa_variant[1], s);
+            e = launch_sweep_aa<double>(sweep_args<double>(ctx, b), b.tiles, pull, ctx->sweep_variant, s);
         else
-            e = launch_sweep_aa<float>(sweep_args<float>(ctx, b), b.tiles, pull, ctx->aa_variant[0], s);
-    } else if (ctx->use_tma) {
-        const CUtensorMap &pm = ctx->tm_pdf[ctx->cur], &psm = ctx->tm_pdfs[ctx->cur];
-        if (ctx->esize == 8)
-            e = launch_sweep_tma<double>(pm, psm, ctx->tm_kind, ctx->tm_flags, sweep_args<double>(ctx, b), b.tiles,
-                                         ctx->num_sms, ctx->tma_variant, s);
-        else
-            e = launch_sweep_tma<float>(pm, psm, ctx->tm_kind, ctx->tm_flags, sweep_args<float>(ctx, b), b.tiles,
-                                        ctx->num_sms, ctx->tma_variant, s);
+            e = launch_sweep_aa<float>(sweep_args<float>(ctx, b), b.tiles, pull, ctx->sweep_variant, s);
     } else if (ctx->esize == 8)
-        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant[1], s);
+        e = launch_sweep<double>(sweep_args<double>(ctx, b), b.tiles, ctx->sweep_variant, s);
     else
-        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, ctx->sweep_variant[0], s);
+        e = launch_sweep<float>(sweep_args<float>(ctx, b), b.tiles, ctx->sweep_variant, s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_kernel launch", __FILE__, __LINE__);
     ctx->launches += 1;
     return LBM_OK;
@@ -82,20 +73,23 @@ lbm_status launch_copy(lbm_ctx *ctx, const DevSegs &d, void *grid_src, void *gri
     return LBM_OK;
 }
 
-// Transport of the send buffers: grouped NCCL send/recv per peer;
-// a self-peer (exchange_mode FORCE_BUFFERS) is a device copy.
+// Transport of the send buffers: grouped NCCL send/recv per peer.
+// A self-peer (exchange_mode FORCE_BUFFERS / SELF_PEER on one GPU) goes through
+// the same NCCL group when the context has a communicator (FORCE_BUFFERS: a
+// one-rank communicator), else (SELF_PEER's state refresh) a device copy.
 lbm_status transport(lbm_ctx *ctx, const ExSet &X, cudaStream_t s)
 {
     const ncclDataType_t dt = ctx->esize == 8 ? ncclFloat64 : ncclFloat32;
     char *sb = (char *)ctx->sendbuf, *rb = (char *)ctx->recvbuf;
-    for (const Peer &p : X.peers)
-        if (p.rank == ctx->dec.rank && p.send_n > 0)
-            CK(cudaMemcpyAsync(rb + p.recv_off * ctx->esize, sb + p.send_off * ctx->esize, p.send_n * ctx->esize,
-                               cudaMemcpyDeviceToDevice, s));
-    if (!X.has_nccl) return LBM_OK;
+    if (!ctx->nccl) {
+        for (const Peer &p : X.peers)
+            if (p.rank == ctx->dec.rank && p.send_n > 0)
+                CK(cudaMemcpyAsync(rb + p.recv_off * ctx->esize, sb + p.send_off * ctx->esize,
+                                   p.send_n * ctx->esize, cudaMemcpyDeviceToDevice, s));
+        return LBM_OK;
+    }
     NK(ncclGroupStart());
     for (const Peer &p : X.peers) {
-        if (p.rank == ctx->dec.rank) continue;
         if (p.send_n > 0) NK(ncclSend(sb + p.send_off * ctx->esize, (size_t)p.send_n, dt, p.rank, ctx->nccl, s));
         if (p.recv_n > 0) NK(ncclRecv(rb + p.recv_off * ctx->esize, (size_t)p.recv_n, dt, p.rank, ctx->nccl, s));
     }
@@ -111,8 +105,8 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, in
     void *grid = ctx->grid[gi];
     const ExSet &X = ctx->ex[kind];
     lbm_status st;
-    // local pull: same-GPU neighbours are read in place, only remote segments move
-    const bool skip_local = ctx->lpull || (in_step && ctx->ldirect);
+    // direct ghost stores: the sweep already filled the same-GPU ghosts
+    const bool skip_local = in_step && ctx->ldirect;
     const bool work = (skip_local ? X.pack_remote.n : X.pack_all.n) > 0 || X.has_remote || X.unpack.n > 0;
     if (!work) return LBM_OK;  // single periodic-free patch: nothing to exchange
     if (ts) ts->exchange = true;
@@ -233,31 +227,20 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         if (e != cudaSuccess) return ctx->cuda_fail(e, "wait_peers launch", __FILE__, __LINE__);
         ctx->launches += 1;
         const DevBoxes &bs = ctx->box_shell;
-        if (bs.tiles > 0 && ctx->x2_shells) {
+        if (bs.tiles > 0) {
             const bool pull = ctx->aa_phase == 0;  // AA: PULL after an even step count
             if (ctx->esize == 8) {
                 SweepArgs<double> a = sweep_args<double>(ctx, bs);
                 a.dnbr = (double *const *)ctx->d_dnbr;
-                e = aa ? launch_sweep_aa<double>(a, bs.tiles, pull, ctx->aa_variant[1], c)
-                       : launch_sweep<double>(a, bs.tiles, ctx->sweep_variant[1], c);
+                e = aa ? launch_sweep_aa<double>(a, bs.tiles, pull, ctx->sweep_variant, c)
+                       : launch_sweep<double>(a, bs.tiles, ctx->sweep_variant, c);
             } else {
                 SweepArgs<float> a = sweep_args<float>(ctx, bs);
                 a.dnbr = (float *const *)ctx->d_dnbr;
-                e = aa ? launch_sweep_aa<float>(a, bs.tiles, pull, ctx->aa_variant[0], c)
-                       : launch_sweep<float>(a, bs.tiles, ctx->sweep_variant[0], c);
+                e = aa ? launch_sweep_aa<float>(a, bs.tiles, pull, ctx->sweep_variant, c)
+                       : launch_sweep<float>(a, bs.tiles, ctx->sweep_variant, c);
             }
             if (e != cudaSuccess) return ctx->cuda_fail(e, "shell sweep launch", __FILE__, __LINE__);
-            ctx->launches += 1;
-        } else if (bs.tiles > 0) {
-            void **tab = ctx->ldirect ? ctx->d_dnbr : ctx->d_nbr;
-            if (ctx->esize == 8) {
-                DirectArgs<double> dx{(double *const *)tab, dsti};
-                e = launch_sweep_direct<double>(sweep_args<double>(ctx, bs), dx, bs.tiles, ctx->direct_variant[1], c);
-            } else {
-                DirectArgs<float> dx{(float *const *)tab, dsti};
-                e = launch_sweep_direct<float>(sweep_args<float>(ctx, bs), dx, bs.tiles, ctx->direct_variant[0], c);
-            }
-            if (e != cudaSuccess) return ctx->cuda_fail(e, "sweep_direct launch", __FILE__, __LINE__);
             ctx->launches += 1;
         }
         e = launch_signal_peers(ctx->d_epoch, ctx->d_peer_inbox, ctx->npeers_direct, c);
@@ -288,7 +271,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
-        if (!ctx->lpull && !ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
+        if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
             return st;
         CK(cudaStreamWaitEvent(s, ts ? ts->ev[11] : ctx->slots[0].ev[11], 0));
     }
@@ -348,6 +331,27 @@ lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n)
             n -= 1;
         }
     }
+    return LBM_OK;
+}
+
+lbm_status quiesce(lbm_ctx *ctx)
+{
+    if (!ctx->direct || ctx->npeers_direct <= 0) return LBM_OK;
+    cudaEvent_t ev = ctx->slots[0].ev[12];
+    CK(cudaEventRecord(ev, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->comm_stream, ev, 0));
+    cudaError_t e = launch_wait_peers(ctx->d_inbox, ctx->d_peer_rank, ctx->npeers_direct, ctx->d_epoch,
+                                      ctx->d_error, ctx->comm_stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "wait_peers launch", __FILE__, __LINE__);
+    ctx->launches += 1;
+    CK(cudaStreamSynchronize(ctx->comm_stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    int err = 0;
+    CK(cudaMemcpy(&err, ctx->d_error, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err)
+        return ctx->fail(LBM_ERR_INTERNAL,
+                         "fused exchange: a peer GPU did not reach the step barrier within LBM_PEER_TIMEOUT_S "
+                         "(default 120 s)");
     return LBM_OK;
 }
 

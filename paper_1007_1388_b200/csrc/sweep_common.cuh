@@ -8,24 +8,51 @@
 
 namespace lbm {
 
-__device__ __forceinline__ int64_t cell_index(const Geom &g, int x, int y, int z)
+// shift of the y / z neighbour of direction i inside a main q-slice (x is handled
+// separately: the x neighbours of the row ends live in the x-ghost columns)
+__device__ __forceinline__ int64_t yz_shift(const Geom &g, int i)
 {
-    return ((int64_t)(z + 1) * g.py + (y + 1)) * (int64_t)g.px + (x + g.xo);
+    return EY(i) * (int64_t)g.px + EZ(i) * g.plane;
 }
+
+// shift of neighbour x + e_i in the flag / kind layout (has an in-row x ghost)
+__device__ __forceinline__ int64_t flag_shift(const Geom &g, int i)
+{
+    return EX(i) + EY(i) * (int64_t)g.fpx + EZ(i) * g.fplane;
+}
+
+// Locate the box and the cell pair of this block / thread: tiles of 64 x 4 cells
+// of one z plane (two cells per thread along x), the box found by a binary
+// search over the tile prefix sums.
+struct PairCoord {
+    int patch, x0, y, z, xend;
+    bool valid;
+};
 
 template <typename real>
-__device__ __forceinline__ real ld_stream(const real *p)
+__device__ __forceinline__ PairCoord locate_pair(const SweepArgs<real> &a)
 {
-    return __ldg(p);
-}
-
-template <typename real, int STCS>
-__device__ __forceinline__ void st_stream(real *p, real v)
-{
-    if (STCS)
-        __stcs(p, v);  // evict-first: dst is not re-read in this sweep
-    else
-        *p = v;
+    const int64_t b = blockIdx.x;
+    int lo = 0, hi = a.nboxes;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
+    }
+    const Box &bx = a.boxes[lo];
+    int t = (int)(b - a.tile_prefix[lo]);
+    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
+    const int tx = t % tiles_x;
+    t /= tiles_x;
+    const int ty = t % tiles_y;
+    const int tz = t / tiles_y;
+    PairCoord c;
+    c.patch = bx.patch;
+    c.x0 = bx.lo[0] + tx * SWEEP_BX + 2 * (int)threadIdx.x;
+    c.y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
+    c.z = bx.lo[2] + tz;
+    c.xend = bx.lo[0] + bx.n[0];
+    c.valid = c.x0 < c.xend && c.y < bx.lo[1] + bx.n[1];
+    return c;
 }
 
 // two cells per thread along x: the 2-vector type of the storage precision

@@ -15,7 +15,7 @@ import numpy as np
 Q = 19
 LBM_FP32, LBM_FP64 = 4, 8
 LBM_FLUID, LBM_NOSLIP, LBM_VELOCITY0 = 0, 1, 2
-LBM_EXCHANGE_AUTO, LBM_EXCHANGE_FORCE_BUFFERS = 0, 1
+LBM_EXCHANGE_AUTO, LBM_EXCHANGE_FORCE_BUFFERS, LBM_EXCHANGE_SELF_PEER = 0, 1, 2
 LBM_LAYOUT_AB, LBM_LAYOUT_AA = 0, 1
 NCCL_ID_BYTES = 128
 NPHASES = 8
@@ -56,7 +56,9 @@ class LbmInfo(ctypes.Structure):
                 ("phase_count", ctypes.c_int64 * NPHASES), ("row_pitch_elems", ctypes.c_int64),
                 ("align_bytes", ctypes.c_int32), ("graphs_active", ctypes.c_int32), ("layout", ctypes.c_int32),
                 ("aa_phase", ctypes.c_int32), ("exchange_fused", ctypes.c_int32),
-                ("local_pull", ctypes.c_int32), ("local_direct", ctypes.c_int32)]
+                ("local_pull", ctypes.c_int32), ("local_direct", ctypes.c_int32),
+                ("overlap_active", ctypes.c_int32), ("nccl_ranks", ctypes.c_int32),
+                ("fused_peers", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
     def to_dict(self) -> dict:
         out = {}
@@ -173,6 +175,14 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _check_out(a, shape, name):
+    """The library writes the whole owned box into caller buffers: refuse anything
+    that is not a C-contiguous float64 array of exactly that shape."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous \
+            or tuple(a.shape) != tuple(shape) or not a.flags.writeable:
+        raise ValueError(f"{name} must be a writeable C-contiguous float64 array of shape {tuple(shape)}")
+
+
 class Lattice:
     """One rank's view of the patch-decomposed lattice (owns an lbm_ctx)."""
 
@@ -264,7 +274,7 @@ class Lattice:
         sx, sy, sz = self.owned_shape
         if out is None:
             out = np.empty((sz, sy, sx, Q), np.float64)
-        assert out.flags.c_contiguous and out.dtype == np.float64 and out.size == sx * sy * sz * Q
+        _check_out(out, (sz, sy, sx, Q), "out")
         self._check(_lib.lbm_get_pdfs(self._ctx, _ptr(out)))
         return out
 
@@ -278,6 +288,8 @@ class Lattice:
         sx, sy, sz = self.owned_shape
         rho = np.empty((sz, sy, sx), np.float64) if rho_out is None else rho_out
         u = np.empty((sz, sy, sx, 3), np.float64) if u_out is None else u_out
+        _check_out(rho, (sz, sy, sx), "rho_out")
+        _check_out(u, (sz, sy, sx, 3), "u_out")
         self._check(_lib.lbm_get_macroscopic(self._ctx, _ptr(rho), _ptr(u)))
         return rho, u
 

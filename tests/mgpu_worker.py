@@ -35,10 +35,9 @@ def main():
     # plus process grids that split x (the driver's 8-GPU run is 2x2x2)
     grids = {2: [(0, 0, 0), (2, 1, 1)], 4: [(0, 0, 0), (2, 2, 1), (2, 1, 2)]}.get(world, [(0, 0, 0)])
     # "fused_copies": fused exchange with same-GPU ghost copies instead of the
-    # sweep's direct ghost stores (LBM_LOCAL_DIRECT=0); "fused_onecell": remote
-    # shells swept by the one-cell sweep_direct_kernel (LBM_SHELL_KERNEL=onecell)
+    # sweep's direct ghost stores (LBM_LOCAL_DIRECT=0)
     combos = [(8, 1, 0, "fused", grids[0]), (4, 1, 0, "fused", grids[0]), (8, 1, 0, "fused_copies", grids[0]),
-              (4, 1, 0, "fused_onecell", grids[0]), (8, 1, 0, "fused_tma", grids[0]),
+              (4, 1, 1, "fused_copies", grids[0]),
               (8, 1, 0, "nccl", grids[0]), (8, 1, 1, "fused", grids[0]), (4, 1, 1, "fused", grids[0]),
               (8, 0, 0, "nccl", grids[0]), (4, 1, 0, "nccl", grids[0]), (8, 1, 1, "nccl", grids[0]),
               (4, 0, 1, "nccl", grids[0])]
@@ -54,14 +53,6 @@ def main():
             os.environ["LBM_LOCAL_DIRECT"] = "0"
         else:
             os.environ.pop("LBM_LOCAL_DIRECT", None)
-        if exch == "fused_onecell":
-            os.environ["LBM_SHELL_KERNEL"] = "onecell"
-        else:
-            os.environ.pop("LBM_SHELL_KERNEL", None)
-        if exch == "fused_tma":  # TMA-staged sweep for the interiors, one-cell fused shells
-            os.environ["LBM_SWEEP_IMPL"] = "tma"
-        else:
-            os.environ.pop("LBM_SWEEP_IMPL", None)
         if True:
             obj = [lbm.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -85,7 +76,7 @@ def main():
                 masses[(prec, overlap, layout, exch, tuple(pgrid))] = mass
                 assert info["exchange_fused"] == (1 if exch.startswith("fused") else 0), info["exchange_fused"]
                 # 8+ patches per rank: same-GPU neighbours take the direct ghost stores
-                assert info["local_direct"] == (0 if exch in ("fused_copies", "fused_tma") else 1), info
+                assert info["local_direct"] == (0 if exch == "fused_copies" else 1), info
                 print(f"prec={prec} overlap={overlap} layout={layout} exchange={exch} peers={info['peers']} "
                       f"halo={info['halo_bytes_remote_per_step']} local_direct={info['local_direct']}", flush=True)
     if rank == 0:

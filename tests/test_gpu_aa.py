@@ -139,7 +139,7 @@ def test_aa_state_rules():
 @pytest.mark.parametrize("prec", [8, 4])
 @pytest.mark.parametrize("n,patch", [((150, 14, 12), None), ((134, 18, 16), (67, 9, 8))])
 def test_aa_variants_bitwise(prec, n, patch, monkeypatch):
-    """Both AA kernel variants (LBM_AA_VARIANT 12 / 13: occupancy targets) and
+    """Both AA kernel variants (LBM_SWEEP_VARIANT 0 / 1: occupancy targets) and
     their straight-line path for wall-free pairs equal the two-grid layout
     bitwise: x extents spanning several 64-cell tiles with a ragged last warp,
     odd patch widths, obstacles on the x faces, two moving walls, periodic y."""
@@ -149,12 +149,12 @@ def test_aa_variants_bitwise(prec, n, patch, monkeypatch):
     wu = np.vstack([wu, [[0.01, 0.0, 0.02]]])
     f0 = inputs.noise_pdfs(n, seed=43)
     out = {}
-    for v in ("12", "13"):
-        monkeypatch.setenv("LBM_AA_VARIANT", v)
+    for v in ("0", "1"):
+        monkeypatch.setenv("LBM_SWEEP_VARIANT", v)
         out[v] = run(n, fl, wu, f0, 10, prec, m.LBM_LAYOUT_AA, patch=patch, periodic=(0, 1, 0))[0]
-    monkeypatch.delenv("LBM_AA_VARIANT")
+    monkeypatch.delenv("LBM_SWEEP_VARIANT")
     ab = run(n, fl, wu, f0, 10, prec, m.LBM_LAYOUT_AB, patch=patch, periodic=(0, 1, 0))[0]
-    for v in ("12", "13"):
+    for v in ("0", "1"):
         np.testing.assert_array_equal(out[v], ab)
 
 

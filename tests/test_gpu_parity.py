@@ -239,48 +239,127 @@ def test_sampled_cells_api():
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_tma_and_simt_sweeps_bitwise_equal(prec, monkeypatch):
-    """The TMA-staged sweep (sweep_tma.cu) and the SIMT sweep share one collide
-    and one store-side bounce-back, so they agree bitwise; patches with ragged
-    sizes, obstacles and a second moving wall, multi-patch exchange."""
+def test_sweep_occupancy_variants_bitwise_equal(prec, monkeypatch):
+    """Both occupancy variants of the x2 sweep (LBM_SWEEP_VARIANT 0 / 1) share one
+    collide and one store-side bounce-back, so they agree bitwise; ragged
+    patches, obstacles and a second moving wall, multi-patch exchange."""
     n = (80, 36, 20)
     fl, wu = inputs.ldc_flags(n, periodic=(0, 1, 0))
     fl = inputs.add_obstacles(fl, 0.04, seed=17, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
     wu = np.vstack([wu, [[0.01, 0.0, -0.02]]])
     f0 = inputs.noise_pdfs(n, seed=19)
     out = {}
-    for impl in ("simt", "tma"):
-        monkeypatch.setenv("LBM_SWEEP_IMPL", impl)
-        out[impl] = run_gpu(n, fl, wu, f0, 13, prec, patch=(40, 18, 10), periodic=(0, 1, 0))
-    np.testing.assert_array_equal(out["tma"], out["simt"])
+    for v in ("0", "1"):
+        monkeypatch.setenv("LBM_SWEEP_VARIANT", v)
+        out[v] = run_gpu(n, fl, wu, f0, 13, prec, patch=(40, 18, 10), periodic=(0, 1, 0))
+    np.testing.assert_array_equal(out["1"], out["0"])
     ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 13, periodic=(0, 1, 0), nthreads=oracle.max_threads())
-    assert max_fluid_diff(out["tma"], ref, fl) <= TOL[prec]
+    assert max_fluid_diff(out["0"], ref, fl) <= TOL[prec]
+
+
+# ---------------------------------------------------------------- the exchange paths on one GPU
+# The multi-GPU exchange paths (NCCL send/recv with the shell / interior overlap,
+# P:287-313 and the overlap the paper did not have, P:603-604; the fused NVLink
+# exchange with its epoch handshake, SURVEY 8(f) NEXT-1) run on one GPU through
+# exchange_mode FORCE_BUFFERS (a one-rank NCCL communicator carries the
+# self-peer messages) and SELF_PEER (this rank is its own fused-exchange peer).
+
+EXCH_CASES = [((36, 30, 24), (12, 10, 8), (0, 1, 0)),   # 3x3x3 ragged patches, periodic y
+              ((64, 16, 12), (64, 16, 12), (1, 1, 1)),  # one fully periodic patch: its own neighbour
+              ((40, 12, 18), (20, 6, 9), (1, 0, 1))]    # 2x2x2 patches, periodic x and z
 
 
 @pytest.mark.parametrize("prec", [8, 4])
-def test_local_pull_equals_ghost_copies(prec, monkeypatch):
-    """Face cells reading same-GPU neighbour patches directly (local pull, NEXT-2)
-    give bitwise the ghost-copy result: 4x3x2 patches, periodic x and z, obstacles
-    on patch boundaries, two moving walls."""
-    n = (64, 30, 24)
-    fl, wu = inputs.ldc_flags(n, periodic=(1, 0, 1))
-    fl = inputs.add_obstacles(fl, 0.06, seed=23, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
-    wu = np.vstack([wu, [[0.0, 0.01, 0.02]]])
-    f0 = inputs.noise_pdfs(n, seed=29)
-    out = {}
-    monkeypatch.setenv("LBM_SWEEP_VARIANT", "5" if prec == 8 else "6")  # local pull is a 1-cell SIMT variant
-    for lp in ("1", "0"):
-        monkeypatch.setenv("LBM_LOCAL_PULL", lp)
-        L = lbm().Lattice(n, (16, 10, 12), inputs.LDC_OMEGA, prec, periodic=(1, 0, 1))
-        assert L.info()["local_pull"] == int(lp)
+@pytest.mark.parametrize("n,patch,periodic", EXCH_CASES)
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_nccl_exchange_one_gpu_vs_oracle(prec, n, patch, periodic, overlap):
+    """FORCE_BUFFERS on one GPU: pack -> grouped ncclSend/ncclRecv through a one-rank
+    communicator -> unpack, with overlap = 1 the shells-first schedule (comm-stream
+    transport and unpack while the interiors are swept).  Element-wise within
+    tolerance of the oracle and bitwise equal to the default exchange."""
+    m = lbm()
+    fl, wu = inputs.ldc_flags(n, periodic=periodic)
+    fl = inputs.add_obstacles(fl, 0.05, seed=51, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.0, 0.01, -0.01]]])
+    f0 = inputs.noise_pdfs(n, seed=53)
+    L = m.Lattice(n, patch, inputs.LDC_OMEGA, prec, periodic=periodic, overlap=overlap,
+                  exchange_mode=m.LBM_EXCHANGE_FORCE_BUFFERS)
+    try:
+        info = L.info()
+        assert info["nccl_ranks"] == 1 and info["exchange_fused"] == 0
+        assert info["overlap_active"] == overlap
         L.set_flags(fl, wu)
         L.set_pdfs(f0)
-        L.step(11)
-        out[lp] = L.get_pdfs()
+        L.set_timing(True)  # one step timed: the overlap branch records its phases
+        L.step(1)
+        ph = L.phase_ms()
+        L.set_timing(False)
+        if overlap:
+            assert ph["sweep_shell"][1] == 1 and ph["sweep_interior"][1] == 1 and ph["nccl"][1] == 1
+        L.step(16)
+        got = L.get_pdfs()
+    finally:
         L.close()
-    np.testing.assert_array_equal(out["1"], out["0"])
-    one = run_gpu(n, fl, wu, f0, 11, prec, periodic=(1, 0, 1))
-    np.testing.assert_array_equal(out["1"], one)
+    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 17, periodic=periodic, nthreads=oracle.max_threads())
+    assert max_fluid_diff(got, ref, fl) <= TOL[prec]
+    np.testing.assert_array_equal(got, run_gpu(n, fl, wu, f0, 17, prec, patch=patch, periodic=periodic))
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("n,patch,periodic", EXCH_CASES)
+def test_fused_exchange_self_peer_vs_oracle(prec, layout, n, patch, periodic):
+    """SELF_PEER on one GPU: the fused multi-GPU exchange -- shells facing the
+    (self-)peer swept on the comm stream with direct stores through the peer
+    table, interiors concurrently on the compute stream, one epoch handshake
+    (wait_peers / signal_peers) per step -- both layouts, odd and even step
+    counts.  Element-wise within tolerance of the oracle, bitwise equal to the
+    default exchange."""
+    m = lbm()
+    fl, wu = inputs.ldc_flags(n, periodic=periodic)
+    fl = inputs.add_obstacles(fl, 0.05, seed=57, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wu = np.vstack([wu, [[0.02, 0.0, 0.01]]])
+    f0 = inputs.noise_pdfs(n, seed=59)
+    L = m.Lattice(n, patch, inputs.LDC_OMEGA, prec, periodic=periodic, layout=layout,
+                  exchange_mode=m.LBM_EXCHANGE_SELF_PEER)
+    try:
+        info = L.info()
+        assert info["exchange_fused"] == 1 and info["fused_peers"] == 1 and info["nccl_ranks"] == 0
+        L.set_flags(fl, wu)
+        L.set_pdfs(f0)
+        L.step(9)
+        odd = L.get_pdfs()
+        L.step(9)
+        got = L.get_pdfs()
+    finally:
+        L.close()
+    ref9 = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 9, periodic=periodic, nthreads=oracle.max_threads())
+    ref = oracle.run(ref9, fl, wu, inputs.LDC_OMEGA, 9, periodic=periodic, nthreads=oracle.max_threads())
+    assert max_fluid_diff(odd, ref9, fl) <= TOL[prec]
+    assert max_fluid_diff(got, ref, fl) <= TOL[prec]
+    np.testing.assert_array_equal(got, run_gpu(n, fl, wu, f0, 18, prec, patch=patch, periodic=periodic))
+
+
+def test_self_peer_quiesce_then_set_pdfs_and_close():
+    """with the fused exchange, state replacement and teardown wait for
+    the peers' last stores.  AA layout, odd step count, then set_pdfs, step and
+    close with no collective in between; the restarted run equals a fresh one."""
+    m = lbm()
+    n, patch = (32, 16, 16), (16, 8, 8)
+    fl, wu = inputs.ldc_flags(n, periodic=(1, 0, 0))
+    f0 = inputs.noise_pdfs(n, seed=61)
+    f1 = inputs.noise_pdfs(n, seed=62)
+    L = m.Lattice(n, patch, inputs.LDC_OMEGA, 8, periodic=(1, 0, 0), layout=1,
+                  exchange_mode=m.LBM_EXCHANGE_SELF_PEER)
+    L.set_flags(fl, wu)
+    L.set_pdfs(f0)
+    L.step_async(5)
+    L.set_pdfs(f1)  # must drain the 5 queued steps and the handshake first
+    L.step(4)
+    got = L.get_pdfs()
+    L.step_async(3)
+    L.close()
+    np.testing.assert_array_equal(got, run_gpu(n, fl, wu, f1, 4, 8, patch=patch, periodic=(1, 0, 0)))
 
 
 @pytest.mark.parametrize("prec", [8, 4])

@@ -12,6 +12,7 @@ int main(void)
     F(lbm_info, owned_lo); F(lbm_info, fluid_cells_local); F(lbm_info, bytes_per_step_algorithmic);
     F(lbm_info, kernel_launches); F(lbm_info, phase_ms); F(lbm_info, phase_count); F(lbm_info, row_pitch_elems);
     F(lbm_info, graphs_active); F(lbm_info, layout); F(lbm_info, aa_phase); F(lbm_info, exchange_fused); F(lbm_info, local_pull); F(lbm_info, local_direct);
+    F(lbm_info, overlap_active); F(lbm_info, nccl_ranks); F(lbm_info, fused_peers);
     F(lbm_msg, dir); F(lbm_msg, nq); F(lbm_msg, cells); F(lbm_msg, offset);
     return 0;
 }

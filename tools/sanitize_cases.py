@@ -1,5 +1,12 @@
-"""Small cases for compute-sanitizer: every sweep variant family once (two-grid
-one/two cells, AA, TMA, local pull), multi-patch with periodic wrap and obstacles."""
+"""Small cases for compute-sanitizer (memcheck / racecheck / initcheck /
+synccheck): every sweep family and exchange path once, in both precisions --
+two grids and AA, both occupancy variants, multi-patch direct ghost stores,
+the NCCL exchange with the shell / interior overlap (FORCE_BUFFERS, one-rank
+communicator) and the fused exchange with its epoch handshake (SELF_PEER),
+with periodic wrap, obstacles on patch faces and two moving walls.
+
+    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+"""
 import os
 import sys
 
@@ -9,21 +16,21 @@ import numpy as np  # noqa: E402
 from paper_1007_1388_b200 import inputs  # noqa: E402
 
 
-def run(layout=0, prec=8, env=None):
+def run(layout=0, prec=8, env=None, exchange_mode=0, n=(36, 21, 13), patches=((36, 21, 13), (36, 7, 13), (18, 7, 13))):
     for k, v in (env or {}).items():
         os.environ[k] = v
     from paper_1007_1388_b200 import lbm
-    n = (37, 21, 13)
     fl, wu = inputs.ldc_flags(n, periodic=(0, 1, 0))
     fl = inputs.add_obstacles(fl, 0.05, seed=3, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
     wu = np.vstack([wu, [[0.0, 0.01, 0.0]]])
-    for patch in ((37, 21, 13), (37, 7, 13)):
-        L = lbm.Lattice(n, patch, 1.3, prec, periodic=(0, 1, 0), layout=layout)
+    for patch in patches:
+        L = lbm.Lattice(n, patch, 1.3, prec, periodic=(0, 1, 0), layout=layout, exchange_mode=exchange_mode)
         L.set_flags(fl, wu)
         L.init_noise(1)
         L.step(3)
         L.get_pdfs()
         L.get_macroscopic()
+        L.total_mass()
         L.close()
     for k in (env or {}):
         os.environ.pop(k)
@@ -31,9 +38,11 @@ def run(layout=0, prec=8, env=None):
 
 if __name__ == "__main__":
     for prec in (8, 4):
-        run(0, prec)
-        run(1, prec)
-        run(0, prec, {"LBM_SWEEP_VARIANT": "5"})
-        run(0, prec, {"LBM_SWEEP_IMPL": "tma"})
-        run(0, prec, {"LBM_SWEEP_VARIANT": "5" if prec == 8 else "6", "LBM_LOCAL_PULL": "1"})
+        for layout in (0, 1):
+            run(layout, prec)                                         # one patch, several, direct stores
+            run(layout, prec, n=(37, 21, 13), patches=((37, 21, 13),))  # odd row length
+            run(layout, prec, exchange_mode=1, patches=((18, 7, 13),))  # NCCL exchange, overlap
+            run(layout, prec, exchange_mode=2, patches=((18, 7, 13),))  # fused exchange, handshake
+        run(0, prec, {"LBM_SWEEP_VARIANT": "1"})
+        run(0, prec, {"LBM_LOCAL_DIRECT": "0"}, patches=((18, 7, 13),))
     print("sanitize cases done")
