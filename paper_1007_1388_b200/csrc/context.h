@@ -27,11 +27,13 @@ constexpr int kTimingSlots = 64;
 enum Phase { PH_SWEEP = 0, PH_SHELL = 1, PH_INTERIOR = 2, PH_PACK = 3, PH_NCCL = 4, PH_UNPACK = 5, PH_STEP = 6 };
 constexpr int kEvPerSlot = 14;
 
+// A sweep's work list: one 16-B descriptor per 64 x 4-cell tile (one block),
+// {patch, x0 << 16 | xend, y0 << 16 | yend, z}, built on the host from the boxes.
+// A block decodes its tile with one load and no division or search.
 struct DevBoxes {
-    Box *boxes = nullptr;
-    int64_t *prefix = nullptr;
-    int n = 0;
-    int64_t tiles = 0;
+    int4 *desc = nullptr;
+    int n = 0;          // boxes
+    int64_t tiles = 0;  // descriptors == blocks of one launch
 };
 
 struct DevSegs {

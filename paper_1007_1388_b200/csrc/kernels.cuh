@@ -24,9 +24,7 @@ struct SweepArgs {
     const real *corr;       // [nvel][19]: 6 w_i rho0 (e_i . u_w[k]) rounded to real
     Geom g;
     real omega;
-    const Box *boxes;       // device
-    const int64_t *tile_prefix; // device, nboxes + 1
-    int nboxes;
+    const int4 *tiles;      // device: one descriptor per block (context.h DevBoxes)
     // Direct ghost stores: [nlocal][18][2] base of the neighbour patch (same GPU,
     // or peer-mapped) in grid i, null where the copy path serves it.  Face / edge
     // cells store their outgoing PDFs into that patch's ghost cells of grid dsti.

@@ -70,7 +70,7 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
                           cfg.patch[a], a, (long long)cfg.domain[a]);
             return g_msg;
         }
-        if (cfg.patch[a] > (1 << 20)) return "patch too large";
+        if (cfg.patch[a] > 32767) return "patch too large (at most 32767 cells per axis: 16-bit tile descriptors)";
         dec.domain[a] = cfg.domain[a];
         dec.patch[a] = cfg.patch[a];
         dec.pgrid[a] = (int)(cfg.domain[a] / cfg.patch[a]);

@@ -50,33 +50,30 @@ Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3])
 
 lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &out)
 {
-    std::vector<int64_t> prefix(boxes.size() + 1, 0);
-    for (size_t i = 0; i < boxes.size(); ++i) {
-        const Box &b = boxes[i];
-        int64_t t = (b.n[0] > 0 && b.n[1] > 0 && b.n[2] > 0) ? (int64_t)b.tiles_x * b.tiles_y * b.n[2] : 0;
-        prefix[i + 1] = prefix[i] + t;
+    std::vector<int4> tiles;
+    for (const Box &b : boxes) {
+        if (b.n[0] <= 0 || b.n[1] <= 0 || b.n[2] <= 0) continue;
+        const int xend = b.lo[0] + b.n[0], yend = b.lo[1] + b.n[1];
+        for (int z = b.lo[2]; z < b.lo[2] + b.n[2]; ++z)
+            for (int ty = 0; ty < b.tiles_y; ++ty)
+                for (int tx = 0; tx < b.tiles_x; ++tx)
+                    tiles.push_back(make_int4(b.patch, ((b.lo[0] + tx * ctx->tile_x) << 16) | xend,
+                                              ((b.lo[1] + ty * ctx->tile_y) << 16) | yend, z));
     }
     out.n = (int)boxes.size();
-    out.tiles = prefix.back();
-    if (boxes.empty()) return LBM_OK;
-    lbm_status st = dev_alloc(ctx, &out.boxes, boxes.size() * sizeof(Box));
+    out.tiles = (int64_t)tiles.size();
+    if (tiles.empty()) return LBM_OK;
+    lbm_status st = dev_alloc(ctx, &out.desc, tiles.size() * sizeof(int4));
     if (st) return st;
-    st = dev_alloc(ctx, &out.prefix, prefix.size() * sizeof(int64_t));
-    if (st) return st;
-    CK(upload(ctx, out.boxes, boxes.data(), boxes.size() * sizeof(Box)));
-    CK(upload(ctx, out.prefix, prefix.data(), prefix.size() * sizeof(int64_t)));
+    CK(upload(ctx, out.desc, tiles.data(), tiles.size() * sizeof(int4)));
     return LBM_OK;
 }
 
 void release_boxes(lbm_ctx *ctx, DevBoxes &b)
 {
-    if (b.boxes) {
-        cudaFree(b.boxes);
-        ctx->device_bytes -= (int64_t)(b.n * sizeof(Box));
-    }
-    if (b.prefix) {
-        cudaFree(b.prefix);
-        ctx->device_bytes -= (int64_t)((b.n + 1) * sizeof(int64_t));
+    if (b.desc) {
+        cudaFree(b.desc);
+        ctx->device_bytes -= (int64_t)(b.tiles * sizeof(int4));
     }
     b = DevBoxes{};
 }
@@ -466,8 +463,7 @@ void destroy_ctx(lbm_ctx *ctx)
             if (p) cudaFree(p);
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
-                    ctx->box_all.boxes, ctx->box_all.prefix, ctx->box_shell.boxes, ctx->box_shell.prefix,
-                    ctx->box_interior.boxes, ctx->box_interior.prefix};
+                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->events_created)

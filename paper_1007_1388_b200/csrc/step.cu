@@ -30,9 +30,7 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.corr = (const real *)ctx->corr;
     a.g = ctx->g;
     a.omega = (real)ctx->cfg.omega;
-    a.boxes = b.boxes;
-    a.tile_prefix = b.prefix;
-    a.nboxes = b.n;
+    a.tiles = b.desc;
     a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
     a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
     return a;

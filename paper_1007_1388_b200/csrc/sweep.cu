@@ -42,9 +42,12 @@ __device__ __forceinline__ void store_bb_ab(const SweepArgs<real> &a, real *D, c
 }
 
 // One thread = the cell pair (x0, x0 + 1) of one row; block (32, 4) threads =
-// 64 x 4 cells of one z plane.  A pair containing a non-fluid cell stores
-// scalars: a wall cell's slots hold store-side bounce-back values of its
-// neighbours and must not be overwritten.
+// 64 x 4 cells of one z plane.  A pair of fluid cells stores 2-vectors; a pair
+// containing a non-fluid cell stores scalars (a wall cell's slots hold
+// store-side bounce-back values of its neighbours and must not be
+// overwritten).  Only lanes next to a wall run the bounce-back stores; keeping
+// that tail small matters because a warp whose row reaches a wall runs it for
+// every lane's instruction stream.
 template <typename real, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)
 {
@@ -69,9 +72,9 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
     const uint32_t m1 = k1 == 1 ? a.wmask[fc + 1] : 0u;
     collide_bgk<real>(p0, a.omega);
     collide_bgk<real>(p1, a.omega);
-    if (k0 == 0 && k1 == 0) {
-        // the common case: both cells fluid with only fluid neighbours
-        real *d = a.dst + (int64_t)pc.patch * g.ps + c;
+    real *d = a.dst + (int64_t)pc.patch * g.ps + c;
+    if (k0 != 2 && k1 != 2) {
+        // both cells fluid (the common case): aligned 2-vector stores
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             V2 w;
@@ -80,21 +83,20 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
             *reinterpret_cast<V2 *>(d + i * g.qs) = w;
         }
     } else {
-        // a non-fluid cell in the pair or a wall next to one: coordinates are
-        // recomputed here rather than kept live through the collision
-        const PairCoord q = locate_pair(a);
-        const int64_t cq = main_index(g, q.x0, q.y, q.z);
-        const int64_t fq = (int64_t)q.patch * g.fs + flag_index(g, q.x0, q.y, q.z);
-        real *D = a.dst + (int64_t)q.patch * g.ps;
-        real *d = D + cq;
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             if (k0 != 2) d[i * g.qs] = p0[i];
             if (k1 != 2) d[i * g.qs + 1] = p1[i];
         }
-        const uint8_t *fl = a.flags + fq;
-        if (m0) store_bb_ab<real>(a, D, fl, q.x0, q.y, q.z, m0, p0);
-        if (m1) store_bb_ab<real>(a, D, fl + 1, q.x0 + 1, q.y, q.z, m1, p1);
+    }
+    if (m0 | m1) {
+        // a wall next to a cell of the pair: coordinates re-decoded from the tile
+        // descriptor (L1 hit) rather than kept live through the collision
+        const PairCoord q = locate_pair(a);
+        const int64_t fq = (int64_t)q.patch * g.fs + flag_index(g, q.x0, q.y, q.z);
+        real *D = a.dst + (int64_t)q.patch * g.ps;
+        if (m0) store_bb_ab<real>(a, D, a.flags + fq, q.x0, q.y, q.z, m0, p0);
+        if (m1) store_bb_ab<real>(a, D, a.flags + fq + 1, q.x0 + 1, q.y, q.z, m1, p1);
     }
     if (DIRECT) direct_stores_x2<real>(a, pc.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);
 }

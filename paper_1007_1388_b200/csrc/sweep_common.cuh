@@ -21,9 +21,9 @@ __device__ __forceinline__ int64_t flag_shift(const Geom &g, int i)
     return EX(i) + EY(i) * (int64_t)g.fpx + EZ(i) * g.fplane;
 }
 
-// Locate the box and the cell pair of this block / thread: tiles of 64 x 4 cells
-// of one z plane (two cells per thread along x), the box found by a binary
-// search over the tile prefix sums.
+// The cell pair of this thread: the block's 64 x 4-cell tile of one z plane
+// from its descriptor (one 16-B load, context.h DevBoxes), two cells per thread
+// along x.
 struct PairCoord {
     int patch, x0, y, z, xend;
     bool valid;
@@ -32,26 +32,14 @@ struct PairCoord {
 template <typename real>
 __device__ __forceinline__ PairCoord locate_pair(const SweepArgs<real> &a)
 {
-    const int64_t b = blockIdx.x;
-    int lo = 0, hi = a.nboxes;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a.tile_prefix[mid] <= b) lo = mid; else hi = mid;
-    }
-    const Box &bx = a.boxes[lo];
-    int t = (int)(b - a.tile_prefix[lo]);
-    const int tiles_x = bx.tiles_x, tiles_y = bx.tiles_y;
-    const int tx = t % tiles_x;
-    t /= tiles_x;
-    const int ty = t % tiles_y;
-    const int tz = t / tiles_y;
+    const int4 t = __ldg(a.tiles + blockIdx.x);
     PairCoord c;
-    c.patch = bx.patch;
-    c.x0 = bx.lo[0] + tx * SWEEP_BX + 2 * (int)threadIdx.x;
-    c.y = bx.lo[1] + ty * SWEEP_BY + (int)threadIdx.y;
-    c.z = bx.lo[2] + tz;
-    c.xend = bx.lo[0] + bx.n[0];
-    c.valid = c.x0 < c.xend && c.y < bx.lo[1] + bx.n[1];
+    c.patch = t.x;
+    c.x0 = (int)((unsigned)t.y >> 16) + 2 * (int)threadIdx.x;
+    c.xend = t.y & 0xffff;
+    c.y = (int)((unsigned)t.z >> 16) + (int)threadIdx.y;
+    c.z = t.w;
+    c.valid = c.x0 < c.xend && c.y < (t.z & 0xffff);
     return c;
 }
 
