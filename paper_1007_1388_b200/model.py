@@ -86,3 +86,23 @@ def b200_step_estimate(brick, proc_coord, proc_grid, s_pdf: int, hbm_gbs: float,
     t = max(t_sweep, t_halo) if overlap else t_sweep + t_halo
     return {"sweep_ms": t_sweep * 1e3, "halo_bytes": hb, "halo_ms": t_halo * 1e3, "step_ms": t * 1e3,
             "mflups": cells / t / 1e6}
+
+
+def hetero_balance(gpu_mflups: float, cpu_mflups: float, n_gpu: int, n_cpu: int, block_cells: int,
+                   gpu_blocks: int | None = None) -> dict:
+    """Static block-count balancing of a heterogeneous GPU + CPU node (P:989-1000,
+    sec:hetero_perf): every CPU process owns one Block, every GPU process b Blocks,
+    and one step takes as long as the slowest process,
+        t = max(b * cells / r_gpu, cells / r_cpu),
+    so the balanced count is b = round(r_gpu / r_cpu) (r_gpu: a GPU process's rate
+    with many Blocks, r_cpu: a CPU process's rate).  Returns b, the step time and
+    the node rate (n_gpu b + n_cpu) cells / t; the exchange overhead the paper
+    names is not modelled.  gpu_blocks overrides b."""
+    b = max(1, round(gpu_mflups / cpu_mflups)) if gpu_blocks is None else gpu_blocks
+    t_gpu = b * block_cells / (gpu_mflups * 1e6)
+    t_cpu = block_cells / (cpu_mflups * 1e6)
+    t = max(t_gpu, t_cpu) if n_cpu else t_gpu
+    cells = (n_gpu * b + n_cpu) * block_cells
+    gpu_only = n_gpu * gpu_mflups
+    return {"gpu_blocks": b, "step_s": t, "node_mflups": cells / t / 1e6, "gpu_only_mflups": gpu_only,
+            "gain": cells / t / 1e6 / gpu_only - 1.0}
