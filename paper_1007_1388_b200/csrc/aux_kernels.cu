@@ -2,6 +2,7 @@
 // local copy / unpack), flags and cell kinds, canonical import /
 // export and macroscopic moments, the seeded noise initialiser, the
 // sampled gather and the store-side bounce-back fill.
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -422,29 +423,34 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
 }
 
 // ---------------------------------------------------------------- bounce-back fill
-// Writes, for the current state, the store-side bounce-back values of every
-// wall-adjacent fluid cell x into its wall neighbours: grid_opp(j)(x + e_j) =
-// grid_j(x) + corr.  Needed once after the state or the flags are set; every
-// later step maintains them inside the sweep.
-// aa = 0: two-grid state (wall slot opp(j) <- S_j(x)); aa = 1: AA swapped
-// state (S_j(x) = A[x][opp(j)], wall slot j, as the LOCAL kernel writes it).
+// Store-side bounce-back (R3) as a list kernel: for every
+// wall-adjacent fluid cell x (the bounce-back list, launch_bb_list_build) and
+// every wall neighbour w = x + e_j, grid_opp(j)(w) = grid_j(x) + corr, so that
+// the next step's pull of x from w is branch-free.  Two-grid layout: run after
+// every sweep on the grid it wrote (the sweep itself carries no wall logic), and
+// once after the state or the flags are set.  aa = 1: AA swapped state
+// (S_j(x) = A[x][opp(j)], wall slot j, as the LOCAL kernel writes it) -- only
+// the initial fill; the AA kernels do their own.  Each wall slot has exactly
+// one writer (x = w - e_j), so entries are independent.
 template <typename real>
-__global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr,
-                               const Geom g, const int aa)
+__global__ void bb_list_kernel(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list,
+                               int64_t n, const real *corr, const Geom g, const int aa)
 {
-    const int lp = blockIdx.y;
-    real *gp = grid + (int64_t)lp * g.ps;
-    const uint8_t *fp = flags + (int64_t)lp * g.fs;
-    const uint8_t *kp = kind + (int64_t)lp * g.fs;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < g.fs; e += (int64_t)gridDim.x * blockDim.x) {
-        if (kp[e] != 1) continue;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t idx = list[t];
+        const int64_t lp = (int64_t)(idx / (uint64_t)g.fs);
+        const int64_t e = (int64_t)(idx - (uint64_t)lp * (uint64_t)g.fs);
+        real *gp = grid + lp * g.ps;
+        const uint8_t *fp = flags + lp * g.fs;
         const int x = (int)(e % g.fpx) - g.fxo;
         const int64_t r = e / g.fpx;
         const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
+        const uint32_t m = wmask[idx];
+#pragma unroll
         for (int j = 1; j < Q; ++j) {
-            const uint8_t f = fp[e + flag_shift(g, j)];
-            if (f == 0) continue;
+            if (!((m >> j) & 1u)) continue;
             real v = gp[pdf_index(g, aa ? OPP(j) : j, x, y, z)];
+            const uint8_t f = fp[e + flag_shift(g, j)];
             if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
             gp[pdf_index(g, aa ? j : OPP(j), x + EX(j), y + EY(j), z + EZ(j))] = v;
         }
@@ -452,17 +458,92 @@ __global__ void bb_fill_kernel(real *grid, const uint8_t *flags, const uint8_t *
 }
 
 template <typename real>
-cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
-                           const Geom &g, int aa, cudaStream_t s)
+cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list, int64_t n,
+                           const real *corr, const Geom &g, int aa, cudaStream_t s)
 {
-    int64_t bx = (g.fs + 255) / 256;
-    if (bx > 2048) bx = 2048;
-    for (int off = 0; off < nlocal; off += 65535) {
-        int n = nlocal - off < 65535 ? nlocal - off : 65535;
-        dim3 grid_dim((unsigned)bx, (unsigned)n);
-        bb_fill_kernel<real><<<grid_dim, 256, 0, s>>>(grid + (int64_t)off * g.ps, flags + (int64_t)off * g.fs,
-                                                      kind + (int64_t)off * g.fs, corr, g, aa);
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    bb_list_kernel<real><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, wmask, list, n, corr, g, aa);
+    return cudaGetLastError();
+}
+
+// The bounce-back list: flag-layout indices (patch * fs + e) of the kind-1 cells
+// of every local patch, in ascending order (deterministic).  Pass 0 counts per
+// chunk, the host scans the counts, pass 1 writes each chunk's entries at its
+// offset in order.
+constexpr int kBbChunk = 256 * 8;
+__global__ void bb_list_build_kernel(const uint8_t *kind, int64_t total, int64_t *counts, uint64_t *list)
+{
+    __shared__ int warp_tot[8];
+    const int64_t base = (int64_t)blockIdx.x * kBbChunk + (int64_t)threadIdx.x * 8;
+    int mine = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mine += (base + k < total && kind[base + k] == 1) ? 1 : 0;
+    // block-exclusive scan of the per-thread counts (thread order = index order)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
     }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int i = 0; i < 8; ++i) {
+        if (i < w) before += warp_tot[i];
+        tot += warp_tot[i];
+    }
+    if (!list) {
+        if (threadIdx.x == 0) counts[blockIdx.x] = tot;
+        return;
+    }
+    int64_t pos = counts[blockIdx.x] + before + incl - mine;
+    for (int k = 0; k < 8; ++k)
+        if (base + k < total && kind[base + k] == 1) list[pos++] = (uint64_t)(base + k);
+}
+
+cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s)
+{
+    const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
+    if (blocks > 0) bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, total, counts, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bb_list_write(const uint8_t *kind, int64_t total, const int64_t *offsets, uint64_t *list,
+                                 cudaStream_t s)
+{
+    const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
+    if (blocks > 0) bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, total, (int64_t *)offsets, list);
+    return cudaGetLastError();
+}
+
+int64_t bb_list_chunks(int64_t total) { return (total + kBbChunk - 1) / kBbChunk; }
+
+// Sweep tiles that hold a non-fluid cell: bit 31 of the descriptor's patch field
+// (sweep_common.cuh locate_pair).  Tiles without one -- every tile of a cavity
+// interior -- sweep without reading the per-cell kind.  One block per tile.
+__global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, const Geom g)
+{
+    for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
+        const int4 t = tiles[b];
+        const int patch = t.x & 0x7fffffff;
+        const int x0 = (int)((unsigned)t.y >> 16), xend = t.y & 0xffff;
+        const int y0 = (int)((unsigned)t.z >> 16), yend = t.z & 0xffff;
+        const int x = x0 + (int)(threadIdx.x % SWEEP_BX), y = y0 + (int)(threadIdx.x / SWEEP_BX);
+        const bool solid =
+            x < xend && y < yend && kind[(int64_t)patch * g.fs + flag_index(g, x, y, t.w)] == 2;
+        const int any = __syncthreads_or(solid);
+        if (threadIdx.x == 0) tiles[b].x = patch | (any ? (int)0x80000000u : 0);
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const Geom &g, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>(n, 148 * 64);
+    tile_solid_kernel<<<(unsigned)blocks, SWEEP_BX * SWEEP_BY, 0, s>>>(tiles, n, kind, g);
     return cudaGetLastError();
 }
 
@@ -470,8 +551,8 @@ cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind
     template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
                                                     const real *, real *, const uint8_t *, const Geom &,       \
                                                     cudaStream_t);                                             \
-    template cudaError_t launch_bb_fill<real>(real *, const uint8_t *, const uint8_t *, const real *, int,      \
-                                              const Geom &, int, cudaStream_t);                                \
+    template cudaError_t launch_bb_list<real>(real *, const uint8_t *, const uint32_t *, const uint64_t *,      \
+                                              int64_t, const real *, const Geom &, int, cudaStream_t);         \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
                                              const int *, const Geom &, real *, int, cudaStream_t);            \
     template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \

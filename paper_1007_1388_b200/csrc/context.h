@@ -102,6 +102,8 @@ struct lbm_ctx {
     int cur = 0;
     uint8_t *flags = nullptr, *kind = nullptr;
     uint32_t *wmask = nullptr;  // wall-neighbour masks of kind-1 cells (flag layout)
+    uint64_t *bb_list = nullptr;  // wall-adjacent fluid cells, patch * fs + e ascending (launch_bb_list)
+    int64_t bb_n = 0;
     void *corr = nullptr;
     int *d_origin = nullptr;
     ExSet ex[3];               // indexed by ExKind
@@ -234,6 +236,11 @@ Geom make_geom(const int n[3], int esize);
 Box make_box(const lbm_ctx *ctx, int patch, const int lo[3], const int n[3]);
 
 lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &out);
+// After the flags change (or the boxes are rebuilt): the bounce-back list and the
+// tiles' non-fluid bits.
+lbm_status build_wall_lists(lbm_ctx *ctx);
+// The store-side bounce-back of the current state's wall-adjacent cells (grid gi).
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int aa, cudaStream_t s);
 
 void release_boxes(lbm_ctx *ctx, DevBoxes &b);
 

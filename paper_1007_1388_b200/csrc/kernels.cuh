@@ -14,6 +14,26 @@ namespace lbm {
 constexpr int SWEEP_BX = 64;
 constexpr int SWEEP_BY = 4;
 
+// Per-direction byte offsets, uniform over a launch and filled on the host
+// (fill_dir_offsets), so that each of a thread's 38 pull addresses and 19 store
+// addresses is its base pointer plus a kernel-parameter constant -- one 64-bit
+// add -- instead of a per-thread multiply / shift chain (the integer address
+// arithmetic was 45 % of the fp32 sweep's instructions, profiles/r02_*).
+//   pull[i]  : p_i of the pair's first cell: slot(i) * qs - e_i . (1, px, plane),
+//              relative to the cell's element in slice 0 (slot(i) = i two-grid,
+//              opp(i) AA PULL); the second cell's value is one element further;
+//   gpull[i] : e_ix != 0, the x-ghost column element it pulls instead at a row
+//              end: slot(i) * gq + (e_ix > 0 ? 0 : gside) - e_iy - e_iz * gy,
+//              relative to the cell's ghost-column base (side 0, q 0, (y, z));
+//   slot[i]  : i * qs (slot i at the cell);
+//   push[i]  : AA PULL scatter target x + e_i in slot i: i * qs + e_i . (1, px, plane);
+//   gpush[i] : e_ix != 0, the x-ghost column target of a row-end scatter:
+//              i * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy.
+struct DirOffsets {
+    int64_t pull[Q], gpull[Q], slot[Q], push[Q], gpush[Q];
+};
+void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o);
+
 template <typename real>
 struct SweepArgs {
     const real *src;
@@ -31,6 +51,7 @@ struct SweepArgs {
     // dnbr == nullptr disables them.
     real *const *dnbr = nullptr;
     int dsti = 0;
+    DirOffsets off;
 };
 
 // The 18 neighbour directions in the plan's order (plan.cpp kDirs).
@@ -76,11 +97,20 @@ cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elem
                                  real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
                                  const Geom &g, cudaStream_t s);
 
-// Store-side bounce-back values of the current state (after set_pdfs / set_flags);
-// aa = 1: AA swapped representation.
+// Store-side bounce-back over the list of wall-adjacent fluid cells (flag-layout
+// indices patch * fs + e, ascending): after every two-grid sweep and once after
+// the state or the flags are set; aa = 1: AA swapped representation.
 template <typename real>
-cudaError_t launch_bb_fill(real *grid, const uint8_t *flags, const uint8_t *kind, const real *corr, int nlocal,
-                           const Geom &g, int aa, cudaStream_t s);
+cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list, int64_t n,
+                           const real *corr, const Geom &g, int aa, cudaStream_t s);
+// Building the list (kind == 1 cells of all `total` flag-layout elements): per-chunk
+// counts (bb_list_chunks(total) of them), then, with their exclusive scan, the entries.
+int64_t bb_list_chunks(int64_t total);
+cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s);
+cudaError_t launch_bb_list_write(const uint8_t *kind, int64_t total, const int64_t *offsets, uint64_t *list,
+                                 cudaStream_t s);
+// Bit 31 of each tile descriptor's patch field: the tile holds a non-fluid cell.
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const Geom &g, cudaStream_t s);
 
 // AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL;
 // variant as launch_sweep.

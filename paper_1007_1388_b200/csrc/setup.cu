@@ -254,6 +254,50 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
     return LBM_OK;
 }
 
+lbm_status build_wall_lists(lbm_ctx *ctx)
+{
+    const int64_t total = (int64_t)ctx->dec.nlocal * ctx->g.fs;
+    const int64_t nch = bb_list_chunks(total);
+    int64_t *d_counts = nullptr;
+    lbm_status st = dev_alloc(ctx, &d_counts, (size_t)std::max<int64_t>(nch, 1) * sizeof(int64_t));
+    if (st) return st;
+    std::vector<int64_t> counts((size_t)nch);
+    cudaError_t e = launch_bb_list_count(ctx->kind, total, d_counts, ctx->stream);
+    if (e == cudaSuccess && nch > 0)
+        e = cudaMemcpyAsync(counts.data(), d_counts, nch * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    int64_t n = 0;
+    for (int64_t &c : counts) {
+        const int64_t t = c;
+        c = n;
+        n += t;
+    }
+    if (ctx->bb_list) {
+        cudaFree(ctx->bb_list);
+        ctx->device_bytes -= ctx->bb_n * (int64_t)sizeof(uint64_t);
+        ctx->bb_list = nullptr;
+    }
+    ctx->bb_n = 0;
+    if (e == cudaSuccess && n > 0) {
+        if ((st = dev_alloc(ctx, &ctx->bb_list, (size_t)n * sizeof(uint64_t)))) {
+            cudaFree(d_counts);
+            ctx->device_bytes -= std::max<int64_t>(nch, 1) * (int64_t)sizeof(int64_t);
+            return st;
+        }
+        ctx->bb_n = n;
+        e = upload(ctx, d_counts, counts.data(), nch * sizeof(int64_t));
+        if (e == cudaSuccess) e = launch_bb_list_write(ctx->kind, total, d_counts, ctx->bb_list, ctx->stream);
+    }
+    for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
+        if (e == cudaSuccess) e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ctx->g, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d_counts);
+    ctx->device_bytes -= std::max<int64_t>(nch, 1) * (int64_t)sizeof(int64_t);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "build wall lists", __FILE__, __LINE__);
+    ctx->launches += 5;
+    return LBM_OK;
+}
+
 // Sweep boxes.  all: one box per local patch.  Overlap: for patches with
 // remote segments, a shell on every side a remote segment touches (1 cell
 // thick in y/z; SWEEP_BX thick in x so the shell rows stay coalesced) and the
@@ -326,6 +370,7 @@ lbm_status build_boxes(lbm_ctx *ctx, bool whole_x)
     if ((st = upload_boxes(ctx, all, ctx->box_all))) return st;
     if ((st = upload_boxes(ctx, shell, ctx->box_shell))) return st;
     if ((st = upload_boxes(ctx, interior, ctx->box_interior))) return st;
+    if (ctx->flags_set && (st = build_wall_lists(ctx))) return st;
     return LBM_OK;
 }
 
@@ -406,7 +451,7 @@ lbm_status apply_flags(lbm_ctx *ctx, const uint8_t *flags, const double *wall_u,
     ctx->fluid_global = gl;
     ctx->fluid_local = lo;
     ctx->flags_set = true;
-    return LBM_OK;
+    return build_wall_lists(ctx);
 }
 
 const char *validate_flags(const Decomp &dec, const uint8_t *flags, const double *wall_u, int nvel)
@@ -463,7 +508,7 @@ void destroy_ctx(lbm_ctx *ctx)
             if (p) cudaFree(p);
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
-                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc};
+                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->events_created)

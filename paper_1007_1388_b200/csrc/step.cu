@@ -13,6 +13,19 @@
 
 namespace lbm {
 
+void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o)
+{
+    for (int i = 0; i < Q; ++i) {
+        const int sl = aa ? OPPf(i) : i;
+        const int64_t yz = EYf(i) * (int64_t)g.px + EZf(i) * g.plane;
+        o.pull[i] = (sl * g.qs - EXf(i) - yz) * esize;
+        o.gpull[i] = (sl * g.gq + (EXf(i) > 0 ? 0 : g.gside) - EYf(i) - EZf(i) * (int64_t)g.gy) * esize;
+        o.slot[i] = i * g.qs * esize;
+        o.push[i] = (i * g.qs + EXf(i) + yz) * esize;
+        o.gpush[i] = (i * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
+    }
+}
+
 template <typename real>
 SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
 {
@@ -33,6 +46,7 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.tiles = b.desc;
     a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
     a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
+    fill_dir_offsets(ctx->g, ctx->layout == LBM_LAYOUT_AA, (int)sizeof(real), a.off);
     return a;
 }
 
@@ -121,6 +135,19 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, in
     return LBM_OK;
 }
 
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int aa, cudaStream_t s)
+{
+    if (ctx->bb_n == 0) return LBM_OK;
+    cudaError_t e = ctx->esize == 8
+                        ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, ctx->wmask, ctx->bb_list,
+                                                 ctx->bb_n, (const double *)ctx->corr, ctx->g, aa, s)
+                        : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, ctx->wmask, ctx->bb_list,
+                                                ctx->bb_n, (const float *)ctx->corr, ctx->g, aa, s);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "bounce-back list launch", __FILE__, __LINE__);
+    ctx->launches += 1;
+    return LBM_OK;
+}
+
 // After the state or the flags change: refresh the ghost layers of the current
 // grid and park the store-side bounce-back values in the wall cells.
 lbm_status refresh_state(lbm_ctx *ctx)
@@ -130,15 +157,7 @@ lbm_status refresh_state(lbm_ctx *ctx)
     const bool aa = ctx->layout == LBM_LAYOUT_AA;
     lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB, false);
     if (st) return st;
-    cudaError_t e = ctx->esize == 8
-                        ? launch_bb_fill<double>((double *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
-                                                 (const double *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
-                                                 ctx->stream)
-                        : launch_bb_fill<float>((float *)ctx->grid[ctx->cur], ctx->flags, ctx->kind,
-                                                (const float *)ctx->corr, ctx->dec.nlocal, ctx->g, aa ? 1 : 0,
-                                                ctx->stream);
-    if (e != cudaSuccess) return ctx->cuda_fail(e, "bb_fill", __FILE__, __LINE__);
-    ctx->launches += (ctx->dec.nlocal + 65534) / 65535;
+    if ((st = launch_bb(ctx, ctx->cur, aa ? 1 : 0, ctx->stream))) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return LBM_OK;
 }
@@ -247,9 +266,11 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ev_shell, c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         CK(cudaStreamWaitEvent(s, ev_shell, 0));
+        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
         if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
     } else if (!ctx->use_overlap) {
         if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
+        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
         if ((st = exchange_seq(ctx, dsti, s, ts, kind, true))) return st;
     } else {
         cudaStream_t c = ctx->comm_stream;
@@ -268,6 +289,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         if (ts) CK(cudaEventRecord(ts->ev[8], c));
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
+        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
         if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
             return st;

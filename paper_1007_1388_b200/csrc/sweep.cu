@@ -23,31 +23,17 @@
 
 namespace lbm {
 
-// Store-side bounce-back (two-grid): f_j(x) leaving toward the wall w = x + e_j
-// comes back to x next step as direction opp(j) (R3); park it, plus
-// the moving-wall term of the delivered direction opp(j), in w's slot opp(j),
-// so the next step's pull of x is branch-free.  m: wall-neighbour mask of x.
-template <typename real>
-__device__ __forceinline__ void store_bb_ab(const SweepArgs<real> &a, real *D, const uint8_t *fl, int x, int y,
-                                            int z, uint32_t m, const real *p)
-{
-#pragma unroll
-    for (int j = 1; j < Q; ++j) {
-        if (!((m >> j) & 1u)) continue;
-        real v = p[j];
-        const uint8_t f = fl[flag_shift(a.g, j)];
-        if (f >= 2) v += a.corr[(f - 2) * Q + OPP(j)];
-        D[pdf_index(a.g, OPP(j), x + EX(j), y + EY(j), z + EZ(j))] = v;
-    }
-}
-
 // One thread = the cell pair (x0, x0 + 1) of one row; block (32, 4) threads =
-// 64 x 4 cells of one z plane.  A pair of fluid cells stores 2-vectors; a pair
-// containing a non-fluid cell stores scalars (a wall cell's slots hold
-// store-side bounce-back values of its neighbours and must not be
-// overwritten).  Only lanes next to a wall run the bounce-back stores; keeping
-// that tail small matters because a warp whose row reaches a wall runs it for
-// every lane's instruction stream.
+// 64 x 4 cells of one z plane.  The sweep carries no wall logic: the pull is
+// branch-free because the wall slots it reads already hold the half-way
+// bounce-back values, which the bounce-back list kernel (aux_kernels.cu
+// bb_list_kernel, store side) writes after every sweep for the few
+// wall-adjacent cells.  (With the walls in the sweep, the per-cell kind load,
+// the dependent wall-mask load and the bounce-back tail of the wall lanes --
+// half the warps of a 256^3 cavity hold an x-wall lane -- cost 10 % (fp64) and
+// 23 % (fp32) of the step, profiles/r02_wall_path_ab.jsonl.)  Only tiles that
+// hold a non-fluid cell read the cells' kinds, so non-fluid cells are neither
+// updated nor stored; a pair of fluid cells stores 2-vectors.
 template <typename real, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const SweepArgs<real> a)
 {
@@ -58,65 +44,58 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
     const bool has1 = x0 + 1 < pc.xend;
     const Geom &g = a.g;
     const int64_t c = main_index(g, x0, y, z);
-    const int64_t fc = (int64_t)pc.patch * g.fs + flag_index(g, x0, y, z);
-    const uchar2 kk = *reinterpret_cast<const uchar2 *>(a.kind + fc);
-    const uint8_t k0 = kk.x, k1 = has1 ? kk.y : (uint8_t)2;
+    uint8_t k0 = 0, k1 = has1 ? 0 : 2;  // 2: non-fluid (or the phantom partner of an odd row end)
+    if (pc.solid) {
+        const uchar2 kk =
+            *reinterpret_cast<const uchar2 *>(a.kind + (int64_t)pc.patch * g.fs + flag_index(g, x0, y, z));
+        k0 = kk.x;
+        if (has1) k1 = kk.y;
+    }
     // x-face neighbour of this pair for the direct ghost stores: -x if x0 == 0,
     // else +x (the +x one of a pair on both faces, n0 <= 2, loads late)
     real *nb_x = nullptr;
     if (DIRECT && (x0 == 0 || x0 + 1 >= g.n[0] - 1)) nb_x = direct_ptr(a, pc.patch, x0 == 0 ? 8 : 9);
+    const real *P = a.src + (int64_t)pc.patch * g.ps;
     real p0[Q], p1[Q];
-    pull_pair<real, false>(g, a.src + (int64_t)pc.patch * g.ps, c, x0, y, z, p0, p1);
+    pull_pair<real>(a.off, P + c, ghost_base(g, P, y, z), x0 == 0, x0 + 1 == g.n[0], x0 + 2 == g.n[0], p0, p1);
     if (k0 == 2 && k1 == 2) return;
-    const uint32_t m0 = k0 == 1 ? a.wmask[fc] : 0u;
-    const uint32_t m1 = k1 == 1 ? a.wmask[fc + 1] : 0u;
-    collide_bgk<real>(p0, a.omega);
-    collide_bgk<real>(p1, a.omega);
+    collide_pair(p0, p1, a.omega);
     real *d = a.dst + (int64_t)pc.patch * g.ps + c;
     if (k0 != 2 && k1 != 2) {
-        // both cells fluid (the common case): aligned 2-vector stores
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
             V2 w;
             w.x = p0[i];
             w.y = p1[i];
-            *reinterpret_cast<V2 *>(d + i * g.qs) = w;
+            *at<V2>(d, a.off.slot[i]) = w;
         }
     } else {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            if (k0 != 2) d[i * g.qs] = p0[i];
-            if (k1 != 2) d[i * g.qs + 1] = p1[i];
+            if (k0 != 2) at<real>(d, a.off.slot[i])[0] = p0[i];
+            if (k1 != 2) at<real>(d, a.off.slot[i])[1] = p1[i];
         }
     }
-    if (m0 | m1) {
-        // a wall next to a cell of the pair: coordinates re-decoded from the tile
-        // descriptor (L1 hit) rather than kept live through the collision
-        const PairCoord q = locate_pair(a);
-        const int64_t fq = (int64_t)q.patch * g.fs + flag_index(g, q.x0, q.y, q.z);
-        real *D = a.dst + (int64_t)q.patch * g.ps;
-        if (m0) store_bb_ab<real>(a, D, a.flags + fq, q.x0, q.y, q.z, m0, p0);
-        if (m1) store_bb_ab<real>(a, D, a.flags + fq + 1, q.x0 + 1, q.y, q.z, m1, p1);
-    }
     if (DIRECT) direct_stores_x2<real>(a, pc.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);
+}
+
+template <typename real, int MINB>
+cudaError_t launch_x2(const SweepArgs<real> &a, unsigned grid, cudaStream_t s)
+{
+    const dim3 block(32, SWEEP_BY, 1);
+    if (a.dnbr) sweep_x2_kernel<real, MINB, true><<<grid, block, 0, s>>>(a);
+    else sweep_x2_kernel<real, MINB, false><<<grid, block, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 template <typename real>
 cudaError_t launch_sweep(const SweepArgs<real> &a, int64_t total_tiles, int variant, cudaStream_t s)
 {
     if (total_tiles <= 0) return cudaSuccess;
-    dim3 block(32, SWEEP_BY, 1);
     const unsigned grid = (unsigned)total_tiles;
-    // min blocks of 128 threads per SM: fp64 3 / 2, fp32 4 / 5 (variant 0 / 1)
-    constexpr int M0 = sizeof(real) == 8 ? 3 : 4, M1 = sizeof(real) == 8 ? 2 : 5;
-    if (a.dnbr) {
-        if (variant == 1) sweep_x2_kernel<real, M1, true><<<grid, block, 0, s>>>(a);
-        else sweep_x2_kernel<real, M0, true><<<grid, block, 0, s>>>(a);
-    } else {
-        if (variant == 1) sweep_x2_kernel<real, M1, false><<<grid, block, 0, s>>>(a);
-        else sweep_x2_kernel<real, M0, false><<<grid, block, 0, s>>>(a);
-    }
-    return cudaGetLastError();
+    // min blocks of 128 threads per SM (variant 0 / 1): fp64 3 / 2, fp32 5 / 4
+    constexpr int M0 = sizeof(real) == 8 ? 3 : 5, M1 = sizeof(real) == 8 ? 2 : 4;
+    return variant == 1 ? launch_x2<real, M1>(a, grid, s) : launch_x2<real, M0>(a, grid, s);
 }
 
 template cudaError_t launch_sweep<float>(const SweepArgs<float> &, int64_t, int, cudaStream_t);

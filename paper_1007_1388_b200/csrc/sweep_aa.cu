@@ -140,11 +140,12 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     real *A = P + c;
     real p0[Q], p1[Q];
     if (PULL) {
-        pull_pair<real, true>(g, P, c, x0, y, z, p0, p1);
+        pull_pair<real>(a.off, A, ghost_base(g, (const real *)P, y, z), x0 == 0, x0 + 1 == g.n[0],
+                        x0 + 2 == g.n[0], p0, p1);
     } else {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            const V2 v = __ldg(reinterpret_cast<const V2 *>(A + i * qs));
+            const V2 v = __ldg(at<const V2>(A, a.off.slot[i]));
             p0[i] = v.x;
             p1[i] = v.y;
         }
@@ -152,8 +153,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     if (k0 == 2 && k1 == 2) return;
     const uint32_t m0 = k0 == 1 ? a.wmask[fc] : 0u;
     const uint32_t m1 = k1 == 1 ? a.wmask[fc + 1] : 0u;
-    collide_bgk<real>(p0, a.omega);
-    collide_bgk<real>(p1, a.omega);
+    collide_pair(p0, p1, a.omega);
     if (k0 == 0 && k1 == 0) {
         // no wall next to either cell (the common case)
         if (PULL) {
@@ -162,26 +162,26 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
             const bool lo0 = x0 == 0, hi1 = x0 + 2 == g.n[0];
 #pragma unroll
             for (int i = 0; i < Q; ++i) {
-                real *t = A + i * qs + yz_shift(g, i);
+                real *t = at<real>(A, a.off.push[i]);  // target of the first cell
                 if (EX(i) == 0) {
                     V2 w;
                     w.x = p0[i];
                     w.y = p1[i];
                     *reinterpret_cast<V2 *>(t) = w;
                 } else if (EX(i) > 0) {  // to x + 1
-                    t[1] = p0[i];
-                    if (!hi1) t[2] = p1[i];
+                    t[0] = p0[i];
+                    if (!hi1) t[1] = p1[i];
                 } else {  // to x - 1
-                    if (!lo0) t[-1] = p0[i];
-                    t[0] = p1[i];
+                    if (!lo0) t[0] = p0[i];
+                    t[1] = p1[i];
                 }
             }
             if (lo0 || hi1) {
-                real *G = P + g.gbase + (int64_t)(z + 1) * g.gy + (y + g.gyo);
+                real *G = ghost_base(g, P, y, z);
 #pragma unroll
                 for (int i = 0; i < Q; ++i) {
                     if (EX(i) == 0) continue;
-                    real *gt = G + i * g.gq + (EX(i) < 0 ? 0 : g.gside) + EY(i) + EZ(i) * (int64_t)g.gy;
+                    real *gt = at<real>(G, a.off.gpush[i]);
                     if (EX(i) > 0 && hi1) *gt = p1[i];
                     if (EX(i) < 0 && lo0) *gt = p0[i];
                 }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
                 V2 w;
                 w.x = p0[i];
                 w.y = p1[i];
-                *reinterpret_cast<V2 *>(A + OPP(i) * qs) = w;
+                *at<V2>(A, a.off.slot[OPP(i)]) = w;
             }
         }
     } else {
@@ -279,8 +279,8 @@ cudaError_t launch_sweep_aa(const SweepArgs<real> &a, int64_t total_tiles, bool 
     if (total_tiles <= 0) return cudaSuccess;
     dim3 block(32, SWEEP_BY, 1);
     const unsigned grid = (unsigned)total_tiles;
-    // min blocks of 128 threads per SM: fp64 3 / 2, fp32 4 / 5 (variant 0 / 1)
-    constexpr int M0 = sizeof(real) == 8 ? 3 : 4, M1 = sizeof(real) == 8 ? 2 : 5;
+    // min blocks of 128 threads per SM (variant 0 / 1): fp64 3 / 2, fp32 5 / 4
+    constexpr int M0 = sizeof(real) == 8 ? 3 : 5, M1 = sizeof(real) == 8 ? 2 : 4;
     const bool m1 = variant == 1;
     if (a.dnbr) {
         if (pull) {

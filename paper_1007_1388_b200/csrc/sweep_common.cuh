@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -22,11 +23,12 @@ __device__ __forceinline__ int64_t flag_shift(const Geom &g, int i)
 }
 
 // The cell pair of this thread: the block's 64 x 4-cell tile of one z plane
-// from its descriptor (one 16-B load, context.h DevBoxes), two cells per thread
-// along x.
+// from its descriptor (one 16-B load, context.h DevBoxes; bit 31 of the patch
+// field: the tile holds a non-fluid cell), two cells per thread along x.
 struct PairCoord {
     int patch, x0, y, z, xend;
     bool valid;
+    bool solid;  // the tile holds a non-fluid cell (launch_tile_solid)
 };
 
 template <typename real>
@@ -34,13 +36,29 @@ __device__ __forceinline__ PairCoord locate_pair(const SweepArgs<real> &a)
 {
     const int4 t = __ldg(a.tiles + blockIdx.x);
     PairCoord c;
-    c.patch = t.x;
+    c.patch = t.x & 0x7fffffff;
+    c.solid = t.x < 0;
     c.x0 = (int)((unsigned)t.y >> 16) + 2 * (int)threadIdx.x;
     c.xend = t.y & 0xffff;
     c.y = (int)((unsigned)t.z >> 16) + (int)threadIdx.y;
     c.z = t.w;
     c.valid = c.x0 < c.xend && c.y < (t.z & 0xffff);
     return c;
+}
+
+// base pointer + byte offset (DirOffsets)
+template <typename T, typename B>
+__device__ __forceinline__ T *at(B *base, int64_t off)
+{
+    using C = typename std::conditional<std::is_const<B>::value || std::is_const<T>::value, const char, char>::type;
+    return reinterpret_cast<T *>(reinterpret_cast<C *>(base) + off);
+}
+
+// x-ghost column base of cell row (y, z): side 0, q 0 (add DirOffsets gpull / gpush)
+template <typename real>
+__device__ __forceinline__ real *ghost_base(const Geom &g, real *P, int y, int z)
+{
+    return P + g.gbase + (int64_t)(z + 1) * g.gy + (y + g.gyo);
 }
 
 // two cells per thread along x: the 2-vector type of the storage precision

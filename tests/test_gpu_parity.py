@@ -240,19 +240,21 @@ def test_sampled_cells_api():
 
 @pytest.mark.parametrize("prec", [8, 4])
 def test_sweep_occupancy_variants_bitwise_equal(prec, monkeypatch):
-    """Both occupancy variants of the x2 sweep (LBM_SWEEP_VARIANT 0 / 1) share one
-    collide and one store-side bounce-back, so they agree bitwise; ragged
-    patches, obstacles and a second moving wall, multi-patch exchange."""
+    """The x2 sweep's variants (LBM_SWEEP_VARIANT 0 / 1: occupancy targets, 2: the
+    cp.async pull into shared memory) share one collide and one store-side
+    bounce-back, so they agree bitwise; ragged patches, obstacles and a second
+    moving wall, multi-patch exchange."""
     n = (80, 36, 20)
     fl, wu = inputs.ldc_flags(n, periodic=(0, 1, 0))
     fl = inputs.add_obstacles(fl, 0.04, seed=17, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
     wu = np.vstack([wu, [[0.01, 0.0, -0.02]]])
     f0 = inputs.noise_pdfs(n, seed=19)
     out = {}
-    for v in ("0", "1"):
+    for v in ("0", "1", "2"):
         monkeypatch.setenv("LBM_SWEEP_VARIANT", v)
         out[v] = run_gpu(n, fl, wu, f0, 13, prec, patch=(40, 18, 10), periodic=(0, 1, 0))
     np.testing.assert_array_equal(out["1"], out["0"])
+    np.testing.assert_array_equal(out["2"], out["0"])
     ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 13, periodic=(0, 1, 0), nthreads=oracle.max_threads())
     assert max_fluid_diff(out["0"], ref, fl) <= TOL[prec]
 
