@@ -156,6 +156,7 @@ LBM_API lbm_status lbm_synchronize(lbm_ctx *ctx)
     // into this rank's grid for every step done have landed.
     lbm_status st = drain(ctx);
     if (st) return st;
+    if ((st = chk_report(ctx))) return st;
     if (ctx->timing) return flush_timing(ctx);
     return LBM_OK;
 }

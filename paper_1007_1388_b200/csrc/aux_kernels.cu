@@ -423,56 +423,82 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
 }
 
 // ---------------------------------------------------------------- bounce-back fill
-// Store-side bounce-back (R3) as a list kernel: for every
-// wall-adjacent fluid cell x (the bounce-back list, launch_bb_list_build) and
-// every wall neighbour w = x + e_j, grid_opp(j)(w) = grid_j(x) + corr, so that
-// the next step's pull of x from w is branch-free.  Two-grid layout: run after
-// every sweep on the grid it wrote (the sweep itself carries no wall logic), and
-// once after the state or the flags are set.  aa = 1: AA swapped state
-// (S_j(x) = A[x][opp(j)], wall slot j, as the LOCAL kernel writes it) -- only
-// the initial fill; the AA kernels do their own.  Each wall slot has exactly
-// one writer (x = w - e_j), so entries are independent.
-template <typename real>
-__global__ void bb_list_kernel(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list,
-                               int64_t n, const real *corr, const Geom g, const int aa)
+// Half-way bounce-back (R3) as a list kernel over the wall-adjacent
+// fluid cells x (the bounce-back list, bb_list_build_kernel) and their wall
+// links w = x + e_j, with corr = 6 w rho0 e_opp(j).u_w of w's velocity:
+//   mode 0 (two grids, after every sweep and once after set_pdfs / set_flags):
+//          grid_opp(j)(w) = grid_j(x) + corr -- store side, so that the next
+//          step's pull of x from w is branch-free;
+//   mode 1 (AA, after LOCAL and once after set_pdfs / set_flags, swapped state
+//          S_j(x) = A[x][opp(j)]): A[w][j] = A[x][opp(j)] + corr;
+//   mode 2 (AA, after PULL, whose straight scatter put out_j(x) into the wall
+//          slot A[w][j]): A[x][opp(j)] = A[w][j] + corr -- the PULL bounce-back.
+// The sweeps themselves carry no wall logic.  Each target slot has exactly one
+// writer (x = w - e_j), so entries are independent.
+template <typename real, int mode>
+__global__ void __launch_bounds__(256, 3) bb_list_kernel(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n,
+                                                      const real *corr, const Geom g, const Checker ck)
 {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t idx = list[t];
-        const int64_t lp = (int64_t)(idx / (uint64_t)g.fs);
-        const int64_t e = (int64_t)(idx - (uint64_t)lp * (uint64_t)g.fs);
+        const BbEntry en = list[t];
+        const int64_t lp = (int64_t)(en.idx / (uint64_t)g.fs);
+        const int64_t e = (int64_t)(en.idx - (uint64_t)lp * (uint64_t)g.fs);
         real *gp = grid + lp * g.ps;
-        const uint8_t *fp = flags + lp * g.fs;
         const int x = (int)(e % g.fpx) - g.fxo;
         const int64_t r = e / g.fpx;
         const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
-        const uint32_t m = wmask[idx];
+        const uint32_t vel = en.vinfo >> 24;
+        // all link values first, then the stores: no slot is both read and
+        // written by this kernel (reads: fluid slots in modes 0 / 1, wall slots in
+        // mode 2; writes: the other kind), so the loads are independent,
+        // non-coherent and in flight together instead of one memory latency per link
+        real v[Q];
 #pragma unroll
         for (int j = 1; j < Q; ++j) {
-            if (!((m >> j) & 1u)) continue;
-            real v = gp[pdf_index(g, aa ? OPP(j) : j, x, y, z)];
-            const uint8_t f = fp[e + flag_shift(g, j)];
-            if (f >= 2) v += corr[(f - 2) * Q + OPP(j)];
-            gp[pdf_index(g, aa ? j : OPP(j), x + EX(j), y + EY(j), z + EZ(j))] = v;
+            if (!((en.mask >> j) & 1u)) continue;
+            const int64_t src = mode == 2 ? pdf_index(g, j, x + EX(j), y + EY(j), z + EZ(j))
+                                          : pdf_index(g, mode == 1 ? OPP(j) : j, x, y, z);
+            v[j] = gld(ck, gp + src);
+        }
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            if (!((en.mask >> j) & 1u)) continue;
+            const int64_t dst = mode == 2 ? pdf_index(g, OPP(j), x, y, z)
+                                          : pdf_index(g, mode == 1 ? j : OPP(j), x + EX(j), y + EY(j), z + EZ(j));
+            real w = v[j];
+            if ((en.vinfo >> j) & 1u) {  // moving wall: its velocity is shared (vel) or read from its flag
+                const int k = vel != kBbMixed ? (int)vel : flags[lp * g.fs + e + flag_shift(g, j)] - 2;
+                w += corr[k * Q + OPP(j)];
+            }
+            gst(ck, gp + dst, w);
+#ifdef LBM_CHECKED
+            if (ck.inject) gst(ck, gp + dst, w);
+#endif
         }
     }
 }
 
 template <typename real>
-cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list, int64_t n,
-                           const real *corr, const Geom &g, int aa, cudaStream_t s)
+cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n, const real *corr,
+                           const Geom &g, int mode, const Checker &ck, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
-    bb_list_kernel<real><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, wmask, list, n, corr, g, aa);
+    if (mode == 2) bb_list_kernel<real, 2><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
+    else if (mode == 1) bb_list_kernel<real, 1><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
+    else bb_list_kernel<real, 0><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
     return cudaGetLastError();
 }
 
-// The bounce-back list: flag-layout indices (patch * fs + e) of the kind-1 cells
-// of every local patch, in ascending order (deterministic).  Pass 0 counts per
-// chunk, the host scans the counts, pass 1 writes each chunk's entries at its
-// offset in order.
+// The bounce-back list: the kind-1 cells of every local patch in ascending
+// flag-layout order (deterministic), each with its wall mask and which of its
+// walls move (and their shared velocity), so the list kernel reads one 16-B
+// entry per cell instead of a mask word and up to 18 flag bytes.  Pass 0
+// counts per chunk, the host scans the counts, pass 1 writes each chunk's
+// entries at its offset in order.
 constexpr int kBbChunk = 256 * 8;
-__global__ void bb_list_build_kernel(const uint8_t *kind, int64_t total, int64_t *counts, uint64_t *list)
+__global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
+                                     const Geom g, int64_t *counts, BbEntry *list)
 {
     __shared__ int warp_tot[8];
     const int64_t base = (int64_t)blockIdx.x * kBbChunk + (int64_t)threadIdx.x * 8;
@@ -499,22 +525,41 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, int64_t total, int64_t
         return;
     }
     int64_t pos = counts[blockIdx.x] + before + incl - mine;
-    for (int k = 0; k < 8; ++k)
-        if (base + k < total && kind[base + k] == 1) list[pos++] = (uint64_t)(base + k);
+    for (int k = 0; k < 8; ++k) {
+        const int64_t i = base + k;
+        if (i >= total || kind[i] != 1) continue;
+        BbEntry en;
+        en.idx = (uint64_t)i;
+        en.mask = wmask[i];
+        uint32_t vm = 0, vel = kBbMixed + 1;  // kBbMixed + 1: no moving wall yet
+        for (int j = 1; j < Q; ++j) {
+            if (!((en.mask >> j) & 1u)) continue;
+            const uint8_t f = flags[i + flag_shift(g, j)];
+            if (f < 2) continue;
+            vm |= 1u << j;
+            const uint32_t kv = f - 2u;
+            vel = vel == kBbMixed + 1 ? kv : (vel == kv ? vel : kBbMixed);
+        }
+        en.vinfo = vm | ((vel > kBbMixed ? 0u : vel) << 24);
+        list[pos++] = en;
+    }
 }
 
 cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
-    if (blocks > 0) bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, total, counts, nullptr);
+    if (blocks > 0)
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, nullptr, nullptr, total, Geom{}, counts, nullptr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bb_list_write(const uint8_t *kind, int64_t total, const int64_t *offsets, uint64_t *list,
-                                 cudaStream_t s)
+cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
+                                 const Geom &g, const int64_t *offsets, BbEntry *list, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
-    if (blocks > 0) bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, total, (int64_t *)offsets, list);
+    if (blocks > 0)
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, flags, total, g, (int64_t *)offsets,
+                                                              list);
     return cudaGetLastError();
 }
 
@@ -551,8 +596,8 @@ cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const
     template cudaError_t launch_copy_segments<real>(const CopySeg *, int, int64_t, const real *, real *,        \
                                                     const real *, real *, const uint8_t *, const Geom &,       \
                                                     cudaStream_t);                                             \
-    template cudaError_t launch_bb_list<real>(real *, const uint8_t *, const uint32_t *, const uint64_t *,      \
-                                              int64_t, const real *, const Geom &, int, cudaStream_t);         \
+    template cudaError_t launch_bb_list<real>(real *, const uint8_t *, const BbEntry *, int64_t, const real *,  \
+                                              const Geom &, int, const Checker &, cudaStream_t);               \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
                                              const int *, const Geom &, real *, int, cudaStream_t);            \
     template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \

@@ -102,7 +102,9 @@ struct lbm_ctx {
     int cur = 0;
     uint8_t *flags = nullptr, *kind = nullptr;
     uint32_t *wmask = nullptr;  // wall-neighbour masks of kind-1 cells (flag layout)
-    uint64_t *bb_list = nullptr;  // wall-adjacent fluid cells, patch * fs + e ascending (launch_bb_list)
+    Checker chk;                  // checked build only (kernels.cuh): shadow arrays of the grids
+    unsigned long long chk_seq = 0;
+    BbEntry *bb_list = nullptr;  // wall-adjacent fluid cells, patch * fs + e ascending (launch_bb_list)
     int64_t bb_n = 0;
     void *corr = nullptr;
     int *d_origin = nullptr;
@@ -239,8 +241,20 @@ lbm_status upload_boxes(lbm_ctx *ctx, const std::vector<Box> &boxes, DevBoxes &o
 // After the flags change (or the boxes are rebuilt): the bounce-back list and the
 // tiles' non-fluid bits.
 lbm_status build_wall_lists(lbm_ctx *ctx);
-// The store-side bounce-back of the current state's wall-adjacent cells (grid gi).
-lbm_status launch_bb(lbm_ctx *ctx, int gi, int aa, cudaStream_t s);
+// Checked build (kernels.cuh Checker): the checker of the next launch (fresh
+// launch sequence), clearing the shadows at a step boundary, and the report
+// (LBM_ERR_INTERNAL with the counts if anything was flagged).  No-ops otherwise.
+Checker next_checker(lbm_ctx *ctx);
+lbm_status chk_alloc(lbm_ctx *ctx, size_t grid_bytes);
+lbm_status chk_clear(lbm_ctx *ctx, cudaStream_t s);
+lbm_status chk_report(lbm_ctx *ctx);
+#ifdef LBM_CHECKED
+constexpr bool kChecked = true;
+#else
+constexpr bool kChecked = false;
+#endif
+// The bounce-back list kernel on grid gi (mode: aux_kernels.cu bb_list_kernel).
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s);
 
 void release_boxes(lbm_ctx *ctx, DevBoxes &b);
 

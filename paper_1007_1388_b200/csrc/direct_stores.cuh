@@ -27,8 +27,8 @@ __device__ __forceinline__ real *direct_ptr(const SweepArgs<real> &a, int patch,
 // pair stays a 2-vector); an x face or an x edge lands in the neighbour's
 // x-ghost column (side 0 of the +x neighbour, side 1 of the -x neighbour).
 template <typename real, int KD, bool OPPSLOT>
-__device__ __forceinline__ void direct_dir_x2(const Geom &g, real *nb, int x0, int y, int z, bool on0, bool on1,
-                                              const real *p0, const real *p1)
+__device__ __forceinline__ void direct_dir_x2(const Geom &g, const Checker &ck, real *nb, int x0, int y, int z, bool on0,
+                                              bool on1, const real *p0, const real *p1)
 {
     using V2 = typename Vec2<real>::T;
     constexpr int ddx = ndir(KD, 0), ddy = ndir(KD, 1), ddz = ndir(KD, 2);
@@ -40,7 +40,7 @@ __device__ __forceinline__ void direct_dir_x2(const Geom &g, real *nb, int x0, i
         const real *pv = on0 ? p0 : p1;
 #pragma unroll
         for (int q = 1; q < Q; ++q)
-            if (outgoing(q, KD)) gc[(OPPSLOT ? OPP(q) : q) * g.gq] = pv[q];
+            if (outgoing(q, KD)) gst(ck, gc + (OPPSLOT ? OPP(q) : q) * g.gq, pv[q]);
     } else {
         real *gb = nb + main_index(g, x0, ty, tz);
 #pragma unroll
@@ -51,10 +51,10 @@ __device__ __forceinline__ void direct_dir_x2(const Geom &g, real *nb, int x0, i
                 V2 w;
                 w.x = p0[q];
                 w.y = p1[q];
-                *reinterpret_cast<V2 *>(gb + sl) = w;
+                gst(ck, reinterpret_cast<V2 *>(gb + sl), w);
             } else {
-                if (on0) gb[sl] = p0[q];
-                if (on1) gb[sl + 1] = p1[q];
+                if (on0) gst(ck, gb + sl, p0[q]);
+                if (on1) gst(ck, gb + sl + 1, p1[q]);
             }
         }
     }
@@ -75,7 +75,7 @@ __device__ __forceinline__ void direct_dir_x2_on(const SweepArgs<real> &a, int p
         on0 = on0 && x0 == n0 - 1;
         on1 = on1 && x0 + 1 == n0 - 1;
     }
-    if (on0 || on1) direct_dir_x2<real, KD, OPPSLOT>(a.g, direct_ptr(a, patch, KD), x0, y, z, on0, on1, p0, p1);
+    if (on0 || on1) direct_dir_x2<real, KD, OPPSLOT>(a.g, a.chk, direct_ptr(a, patch, KD), x0, y, z, on0, on1, p0, p1);
 }
 
 template <typename real, bool OPPSLOT, int... KD>
@@ -107,10 +107,10 @@ __device__ __forceinline__ void direct_stores_x2(const SweepArgs<real> &a, int p
     if (!yzf) {
         const bool hi0 = c0 && x0 == n0 - 1, hi1 = c1 && x0 + 1 == n0 - 1;
         if (x0 == 0) {
-            direct_dir_x2<real, 8, OPPSLOT>(g, nb_x, x0, y, z, c0, false, p0, p1);
-            if (hi0 || hi1) direct_dir_x2<real, 9, OPPSLOT>(g, direct_ptr(a, patch, 9), x0, y, z, hi0, hi1, p0, p1);
+            direct_dir_x2<real, 8, OPPSLOT>(g, a.chk, nb_x, x0, y, z, c0, false, p0, p1);
+            if (hi0 || hi1) direct_dir_x2<real, 9, OPPSLOT>(g, a.chk, direct_ptr(a, patch, 9), x0, y, z, hi0, hi1, p0, p1);
         } else {
-            direct_dir_x2<real, 9, OPPSLOT>(g, nb_x, x0, y, z, hi0, hi1, p0, p1);
+            direct_dir_x2<real, 9, OPPSLOT>(g, a.chk, nb_x, x0, y, z, hi0, hi1, p0, p1);
         }
         return;
     }

@@ -26,13 +26,39 @@ constexpr int SWEEP_BY = 4;
 //              end: slot(i) * gq + (e_ix > 0 ? 0 : gside) - e_iy - e_iz * gy,
 //              relative to the cell's ghost-column base (side 0, q 0, (y, z));
 //   slot[i]  : i * qs (slot i at the cell);
+//   oslot[i] : opp(i) * qs (AA LOCAL's stores; a separate table so that ptxas
+//              re-derives the store addresses instead of keeping the 19 load
+//              addresses live through the collision);
 //   push[i]  : AA PULL scatter target x + e_i in slot i: i * qs + e_i . (1, px, plane);
 //   gpush[i] : e_ix != 0, the x-ghost column target of a row-end scatter:
 //              i * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy.
 struct DirOffsets {
-    int64_t pull[Q], gpull[Q], slot[Q], push[Q], gpush[Q];
+    int64_t pull[Q], gpull[Q], slot[Q], oslot[Q], push[Q], gpush[Q];
 };
 void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o);
+
+// Checked build (make checked, -DLBM_CHECKED; tools/check_cases.py): every
+// global load / store of the sweeps, the direct ghost stores and the bounce-back
+// list is checked to lie inside the PDF grid allocations, and shadow arrays
+// record per element the last writer and reader (id = launch sequence << 32 |
+// thread + 1) over one time step.  Counted errors: [0] an access outside the
+// grids or misaligned, [1] an element written twice in one step (the
+// single-writer claim), [2] an element read by one thread and written by
+// another in the same launch (a race of the in-place AA kernels).  The
+// product build carries an empty Checker.
+#ifdef LBM_CHECKED
+struct Checker {
+    const char *lo[2] = {nullptr, nullptr}, *hi[2] = {nullptr, nullptr};
+    unsigned long long *wr = nullptr, *rd = nullptr;  // [2][elems]
+    unsigned long long *err = nullptr;                  // [3]
+    int64_t elems = 0;                                  // elements per grid
+    int esize = 8;
+    int inject = 0;  // LBM_CHECKED_INJECT=1: the bounce-back list stores twice (the checker's negative control)
+    unsigned long long launch = 0;
+};
+#else
+struct Checker {};
+#endif
 
 template <typename real>
 struct SweepArgs {
@@ -52,6 +78,7 @@ struct SweepArgs {
     real *const *dnbr = nullptr;
     int dsti = 0;
     DirOffsets off;
+    Checker chk;
 };
 
 // The 18 neighbour directions in the plan's order (plan.cpp kDirs).
@@ -97,18 +124,27 @@ cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elem
                                  real *grid_dst, const real *buf_src, real *buf_dst, const uint8_t *flags,
                                  const Geom &g, cudaStream_t s);
 
-// Store-side bounce-back over the list of wall-adjacent fluid cells (flag-layout
-// indices patch * fs + e, ascending): after every two-grid sweep and once after
-// the state or the flags are set; aa = 1: AA swapped representation.
+// Half-way bounce-back over the list of wall-adjacent fluid cells (modes in
+// aux_kernels.cu bb_list_kernel: 0 two-grid store side, 1 AA LOCAL store side /
+// swapped state, 2 AA PULL fix-up), after every sweep and once after the state
+// or the flags are set.  One entry per cell: its flag-layout index
+// (patch * fs + e, ascending), wall mask (bit j: x + e_j is non-fluid) and
+// vinfo = bits j of the moving walls | their shared velocity index << 24
+// (kBbMixed: the walls move differently -- read each wall's flag).
+struct BbEntry {
+    uint64_t idx;
+    uint32_t mask, vinfo;
+};
+constexpr uint32_t kBbMixed = 255;
 template <typename real>
-cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const uint32_t *wmask, const uint64_t *list, int64_t n,
-                           const real *corr, const Geom &g, int aa, cudaStream_t s);
+cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n, const real *corr,
+                           const Geom &g, int mode, const Checker &ck, cudaStream_t s);
 // Building the list (kind == 1 cells of all `total` flag-layout elements): per-chunk
 // counts (bb_list_chunks(total) of them), then, with their exclusive scan, the entries.
 int64_t bb_list_chunks(int64_t total);
 cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s);
-cudaError_t launch_bb_list_write(const uint8_t *kind, int64_t total, const int64_t *offsets, uint64_t *list,
-                                 cudaStream_t s);
+cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
+                                 const Geom &g, const int64_t *offsets, BbEntry *list, cudaStream_t s);
 // Bit 31 of each tile descriptor's patch field: the tile holds a non-fluid cell.
 cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const Geom &g, cudaStream_t s);
 

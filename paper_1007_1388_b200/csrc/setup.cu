@@ -256,6 +256,14 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
 
 lbm_status build_wall_lists(lbm_ctx *ctx)
 {
+    // The captured step graphs hold the old list's pointer and length: drop them
+    // (the next multi-step call re-captures).
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 2; ++i)
+        if (ctx->graph[i]) {
+            cudaGraphExecDestroy(ctx->graph[i]);
+            ctx->graph[i] = nullptr;
+        }
     const int64_t total = (int64_t)ctx->dec.nlocal * ctx->g.fs;
     const int64_t nch = bb_list_chunks(total);
     int64_t *d_counts = nullptr;
@@ -274,19 +282,21 @@ lbm_status build_wall_lists(lbm_ctx *ctx)
     }
     if (ctx->bb_list) {
         cudaFree(ctx->bb_list);
-        ctx->device_bytes -= ctx->bb_n * (int64_t)sizeof(uint64_t);
+        ctx->device_bytes -= ctx->bb_n * (int64_t)sizeof(BbEntry);
         ctx->bb_list = nullptr;
     }
     ctx->bb_n = 0;
     if (e == cudaSuccess && n > 0) {
-        if ((st = dev_alloc(ctx, &ctx->bb_list, (size_t)n * sizeof(uint64_t)))) {
+        if ((st = dev_alloc(ctx, &ctx->bb_list, (size_t)n * sizeof(BbEntry)))) {
             cudaFree(d_counts);
             ctx->device_bytes -= std::max<int64_t>(nch, 1) * (int64_t)sizeof(int64_t);
             return st;
         }
         ctx->bb_n = n;
         e = upload(ctx, d_counts, counts.data(), nch * sizeof(int64_t));
-        if (e == cudaSuccess) e = launch_bb_list_write(ctx->kind, total, d_counts, ctx->bb_list, ctx->stream);
+        if (e == cudaSuccess)
+            e = launch_bb_list_write(ctx->kind, ctx->wmask, ctx->flags, total, ctx->g, d_counts, ctx->bb_list,
+                                     ctx->stream);
     }
     for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
         if (e == cudaSuccess) e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ctx->g, ctx->stream);
@@ -508,7 +518,11 @@ void destroy_ctx(lbm_ctx *ctx)
             if (p) cudaFree(p);
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
-                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list};
+                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list
+#ifdef LBM_CHECKED
+                    , ctx->chk.wr, ctx->chk.rd, ctx->chk.err
+#endif
+    };
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (ctx->events_created)
@@ -747,6 +761,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if ((st = dev_alloc(ctx, &ctx->grid[i], grid_bytes))) return bail(st);
         if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
     }
+    if ((st = chk_alloc(ctx, grid_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->wmask, flag_bytes * sizeof(uint32_t)))) return bail(st);

@@ -5,6 +5,7 @@
 // (P:287-313), shells first and overlapped with the interiors (the
 // paper sums these times).  Step pairs are captured in CUDA graphs.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <new>
@@ -21,9 +22,77 @@ void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o)
         o.pull[i] = (sl * g.qs - EXf(i) - yz) * esize;
         o.gpull[i] = (sl * g.gq + (EXf(i) > 0 ? 0 : g.gside) - EYf(i) - EZf(i) * (int64_t)g.gy) * esize;
         o.slot[i] = i * g.qs * esize;
+        o.oslot[i] = OPPf(i) * g.qs * esize;
         o.push[i] = (i * g.qs + EXf(i) + yz) * esize;
         o.gpush[i] = (i * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
     }
+}
+
+Checker next_checker(lbm_ctx *ctx)
+{
+    Checker c = ctx->chk;
+#ifdef LBM_CHECKED
+    c.launch = (++ctx->chk_seq) << 32;
+#endif
+    return c;
+}
+
+lbm_status chk_alloc(lbm_ctx *ctx, size_t grid_bytes)
+{
+#ifdef LBM_CHECKED
+    Checker &c = ctx->chk;
+    c.esize = ctx->esize;
+    if (const char *v = std::getenv("LBM_CHECKED_INJECT")) c.inject = std::atoi(v);
+    c.elems = (int64_t)(grid_bytes / ctx->esize);
+    for (int i = 0; i < 2; ++i) {
+        c.lo[i] = (const char *)ctx->grid[i];
+        c.hi[i] = ctx->grid[i] ? (const char *)ctx->grid[i] + grid_bytes : nullptr;
+    }
+    lbm_status st;
+    if ((st = dev_alloc(ctx, &c.wr, 2 * (size_t)c.elems * sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &c.rd, 2 * (size_t)c.elems * sizeof(unsigned long long)))) return st;
+    if ((st = dev_alloc(ctx, &c.err, 3 * sizeof(unsigned long long)))) return st;
+    CK(memset_sync(ctx, c.err, 0, 3 * sizeof(unsigned long long)));
+    return chk_clear(ctx, ctx->stream);
+#else
+    (void)ctx;
+    (void)grid_bytes;
+    return LBM_OK;
+#endif
+}
+
+lbm_status chk_clear(lbm_ctx *ctx, cudaStream_t s)
+{
+#ifdef LBM_CHECKED
+    const size_t b = 2 * (size_t)ctx->chk.elems * sizeof(unsigned long long);
+    CK(cudaMemsetAsync(ctx->chk.wr, 0, b, s));
+    CK(cudaMemsetAsync(ctx->chk.rd, 0, b, s));
+#else
+    (void)ctx;
+    (void)s;
+#endif
+    return LBM_OK;
+}
+
+lbm_status chk_report(lbm_ctx *ctx)
+{
+#ifdef LBM_CHECKED
+    unsigned long long e[3] = {0, 0, 0};
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(e, ctx->chk.err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e[0] | e[1] | e[2]) {
+        CK(cudaMemset(ctx->chk.err, 0, sizeof e));
+        char buf[256];
+        std::snprintf(buf, sizeof buf,
+                      "checked build: %llu out-of-bounds or misaligned accesses, %llu elements written twice in "
+                      "one step, %llu read/write races within a launch",
+                      e[0], e[1], e[2]);
+        return ctx->fail(LBM_ERR_INTERNAL, buf);
+    }
+#else
+    (void)ctx;
+#endif
+    return LBM_OK;
 }
 
 template <typename real>
@@ -47,6 +116,7 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
     a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
     fill_dir_offsets(ctx->g, ctx->layout == LBM_LAYOUT_AA, (int)sizeof(real), a.off);
+    a.chk = next_checker(ctx);
     return a;
 }
 
@@ -135,14 +205,14 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, in
     return LBM_OK;
 }
 
-lbm_status launch_bb(lbm_ctx *ctx, int gi, int aa, cudaStream_t s)
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s)
 {
     if (ctx->bb_n == 0) return LBM_OK;
     cudaError_t e = ctx->esize == 8
-                        ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, ctx->wmask, ctx->bb_list,
-                                                 ctx->bb_n, (const double *)ctx->corr, ctx->g, aa, s)
-                        : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, ctx->wmask, ctx->bb_list,
-                                                ctx->bb_n, (const float *)ctx->corr, ctx->g, aa, s);
+                        ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
+                                                 (const double *)ctx->corr, ctx->g, mode, next_checker(ctx), s)
+                        : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
+                                                (const float *)ctx->corr, ctx->g, mode, next_checker(ctx), s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "bounce-back list launch", __FILE__, __LINE__);
     ctx->launches += 1;
     return LBM_OK;
@@ -157,9 +227,10 @@ lbm_status refresh_state(lbm_ctx *ctx)
     const bool aa = ctx->layout == LBM_LAYOUT_AA;
     lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB, false);
     if (st) return st;
+    if ((st = chk_clear(ctx, ctx->stream))) return st;
     if ((st = launch_bb(ctx, ctx->cur, aa ? 1 : 0, ctx->stream))) return st;
     CK(cudaStreamSynchronize(ctx->stream));
-    return LBM_OK;
+    return chk_report(ctx);
 }
 
 lbm_status accumulate_slot(lbm_ctx *ctx, TimingSlot &ts)
@@ -212,6 +283,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
     cudaStream_t s = ctx->stream;
     TimingSlot *ts = nullptr;
     lbm_status st;
+    if (kChecked && (st = chk_clear(ctx, s))) return st;  // one step = one single-writer window
     if (ctx->timing) {
         ts = &ctx->slots[ctx->slot_next];
         ctx->slot_next = (ctx->slot_next + 1) % kTimingSlots;
@@ -228,6 +300,9 @@ lbm_status enqueue_step(lbm_ctx *ctx)
     const int kind = aa ? (ctx->aa_phase == 0 ? EX_AA2 : EX_AA1) : EX_AB;
     const ExSet &X = ctx->ex[kind];
     void *dst = ctx->grid[dsti];
+    // walls after the sweep (launch_bb_list): two grids store-side (0); AA: the
+    // PULL fix-up (2) or LOCAL's store side (1)
+    const int bb_mode = aa ? (ctx->aa_phase == 0 ? 2 : 1) : 0;
     if (ctx->direct) {
         // Fused exchange across GPUs.  C (high priority): wait for the peers' epoch,
         // sweep the shells facing remote neighbours with the fused kernel (NVLink
@@ -266,11 +341,11 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         CK(cudaEventRecord(ev_shell, c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
         CK(cudaStreamWaitEvent(s, ev_shell, 0));
-        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
+        if ((st = launch_bb(ctx, dsti, bb_mode, s))) return st;
         if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s))) return st;
     } else if (!ctx->use_overlap) {
         if ((st = launch_sweep_set(ctx, ctx->box_all, s))) return st;
-        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
+        if ((st = launch_bb(ctx, dsti, bb_mode, s))) return st;
         if ((st = exchange_seq(ctx, dsti, s, ts, kind, true))) return st;
     } else {
         cudaStream_t c = ctx->comm_stream;
@@ -289,7 +364,7 @@ lbm_status enqueue_step(lbm_ctx *ctx)
         if (ts) CK(cudaEventRecord(ts->ev[8], c));
         CK(cudaEventRecord(ts ? ts->ev[11] : ctx->slots[0].ev[11], c));
         if ((st = launch_sweep_set(ctx, ctx->box_interior, s))) return st;
-        if (!aa && (st = launch_bb(ctx, dsti, 0, s))) return st;
+        if ((st = launch_bb(ctx, dsti, bb_mode, s))) return st;
         if (ts) CK(cudaEventRecord(ts->ev[9], s));
         if (!ctx->ldirect && (st = launch_copy(ctx, X.local_copy, dst, dst, nullptr, nullptr, s)))
             return st;
@@ -336,7 +411,7 @@ lbm_status ensure_graph(lbm_ctx *ctx)
 lbm_status enqueue_steps(lbm_ctx *ctx, int64_t n)
 {
     lbm_status st;
-    const bool graphs = ctx->cfg.use_graphs && !ctx->timing;
+    const bool graphs = ctx->cfg.use_graphs && !ctx->timing && !kChecked;
     const bool aa = ctx->layout == LBM_LAYOUT_AA;
     while (n > 0) {
         if (graphs && n >= 2 && !(aa && ctx->aa_phase != 0)) {

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
     if (DIRECT && (x0 == 0 || x0 + 1 >= g.n[0] - 1)) nb_x = direct_ptr(a, pc.patch, x0 == 0 ? 8 : 9);
     const real *P = a.src + (int64_t)pc.patch * g.ps;
     real p0[Q], p1[Q];
-    pull_pair<real>(a.off, P + c, ghost_base(g, P, y, z), x0 == 0, x0 + 1 == g.n[0], x0 + 2 == g.n[0], p0, p1);
+    pull_pair<real>(a.off, a.chk, P + c, ghost_base(g, P, y, z), x0 == 0, x0 + 1 == g.n[0], x0 + 2 == g.n[0], p0, p1);
     if (k0 == 2 && k1 == 2) return;
     collide_pair(p0, p1, a.omega);
     real *d = a.dst + (int64_t)pc.patch * g.ps + c;
@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
             V2 w;
             w.x = p0[i];
             w.y = p1[i];
-            *at<V2>(d, a.off.slot[i]) = w;
+            gst(a.chk, at<V2>(d, a.off.slot[i]), w);
         }
     } else {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            if (k0 != 2) at<real>(d, a.off.slot[i])[0] = p0[i];
-            if (k1 != 2) at<real>(d, a.off.slot[i])[1] = p1[i];
+            if (k0 != 2) gst(a.chk, at<real>(d, a.off.slot[i]), p0[i]);
+            if (k1 != 2) gst(a.chk, at<real>(d, a.off.slot[i]) + 1, p1[i]);
         }
     }
     if (DIRECT) direct_stores_x2<real>(a, pc.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);

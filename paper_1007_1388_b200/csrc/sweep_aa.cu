@@ -19,11 +19,12 @@
 // Two cells per thread along x (cf. sweep_x2_kernel): LOCAL reads and writes
 // only its own cells, so all 19 loads and 19 stores are aligned 2-vectors; PULL
 // vectorises the 9 gathers and scatters with e_x = 0, and its row-end cells
-// gather from / scatter into the x-ghost columns.  Pairs with no wall next to
-// either cell (kind 0, the common case) take a straight-line scatter: the
-// per-direction redirect tests cost PULL +41 % instructions in this
-// latency-bound kernel (1.05 -> 0.88 ms at 256^3 fp64, round 1,
-// profiles/r01_ncu_aa_*).
+// gather from / scatter into the x-ghost columns.  Every pair of fluid cells
+// takes a straight-line scatter: per-direction wall redirect tests cost PULL
+// +41 % instructions (1.05 -> 0.88 ms at 256^3 fp64, round 1,
+// profiles/r01_ncu_aa_*), and the walls' dependent mask loads and bounce-back
+// tails a further 10-20 % (round 2) -- both now live in the bounce-back list
+// kernel that runs after each AA step (sweep_aa_x2_kernel below).
 //
 // Direct ghost stores (the AA pattern's two half-exchanges folded into the
 // sweep):
@@ -50,11 +51,12 @@ namespace lbm {
 __constant__ int8_t c_kd27[27] = {-1, 0,  -1, 1,  2,  3,  -1, 4,  -1, 5,  6,  7,  8, -1,
                                   9,  10, 11, 12, -1, 13, -1, 14, 15, 16, -1, 17, -1};
 
-// PULL of one cell on a y / z face: every scatter target x + e_q outside the patch
-// that is not a wall goes into the neighbour patch holding it.
+// PULL of one cell on a y / z face: every scatter target x + e_q outside the
+// patch goes into the neighbour patch holding it.  A wall target receives the
+// value too (never read there: the bounce-back list's fix-up takes it from this
+// patch's own ghost copy, which the straight scatter also wrote).
 template <typename real>
-__device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int patch, int x, int y, int z, uint32_t m,
-                                               const real *p)
+__device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int patch, int x, int y, int z, const real *p)
 {
     const Geom &g = a.g;
     const int n0 = g.n[0], n1 = g.n[1], n2 = g.n[2];
@@ -65,11 +67,10 @@ __device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int pat
         const int oy = dy < 0 ? -1 : (dy >= n1 ? 1 : 0);
         const int oz = dz < 0 ? -1 : (dz >= n2 ? 1 : 0);
         if ((ox | oy | oz) == 0) continue;  // target inside the patch
-        if ((m >> q) & 1u) continue;        // wall target: the bounce-back stays at x
         const int kd = c_kd27[(oz + 1) * 9 + (oy + 1) * 3 + (ox + 1)];
         real *nb = direct_ptr(a, patch, kd);
         if (!nb) continue;
-        nb[pdf_index(g, q, dx - ox * n0, dy - oy * n1, dz - oz * n2)] = p[q];
+        gst(a.chk, nb + pdf_index(g, q, dx - ox * n0, dy - oy * n1, dz - oz * n2), p[q]);
     }
 }
 
@@ -77,8 +78,7 @@ __device__ __forceinline__ void aa_pull_direct(const SweepArgs<real> &a, int pat
 // targets x + e_q with e_qx = S are the x neighbour's cells
 // (x + S - S n0, y + e_qy, z + e_qz); y +- 1, z +- 1 stay inside the patch.
 template <typename real, int S>
-__device__ __forceinline__ void aa_pull_xface(const SweepArgs<real> &a, real *nb, int x, int y, int z, uint32_t m,
-                                              const real *p)
+__device__ __forceinline__ void aa_pull_xface(const SweepArgs<real> &a, real *nb, int x, int y, int z, const real *p)
 {
     if (!nb) return;
     const Geom &g = a.g;
@@ -86,8 +86,7 @@ __device__ __forceinline__ void aa_pull_xface(const SweepArgs<real> &a, real *nb
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
         if (EXf(q) != S) continue;
-        if ((m >> q) & 1u) continue;  // wall target: the bounce-back stays at x
-        row[q * g.qs + yz_shift(g, q)] = p[q];
+        gst(a.chk, row + q * g.qs + yz_shift(g, q), p[q]);
     }
 }
 
@@ -95,8 +94,7 @@ __device__ __forceinline__ void aa_pull_xface(const SweepArgs<real> &a, real *nb
 // neighbour of the pair's x-face cell (-x if x0 == 0, else +x), loaded up front.
 template <typename real, bool PULL>
 __device__ __forceinline__ void aa_direct_pair(const SweepArgs<real> &a, int patch, int x0, int y, int z, bool has1,
-                                               uint8_t k0, uint8_t k1, uint32_t m0, uint32_t m1, const real *p0,
-                                               const real *p1, real *nb_x)
+                                               uint8_t k0, uint8_t k1, const real *p0, const real *p1, real *nb_x)
 {
     if (!PULL) {
         direct_stores_x2<real, true>(a, patch, x0, y, z, k0 != 2, has1 && k1 != 2, p0, p1, nb_x);
@@ -106,20 +104,28 @@ __device__ __forceinline__ void aa_direct_pair(const SweepArgs<real> &a, int pat
     const int n0 = g.n[0];
     const bool yzf = y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1;  // warp-uniform
     if (yzf) {
-        if (k0 != 2) aa_pull_direct<real>(a, patch, x0, y, z, m0, p0);
-        if (has1 && k1 != 2) aa_pull_direct<real>(a, patch, x0 + 1, y, z, m1, p1);
+        if (k0 != 2) aa_pull_direct<real>(a, patch, x0, y, z, p0);
+        if (has1 && k1 != 2) aa_pull_direct<real>(a, patch, x0 + 1, y, z, p1);
         return;
     }
     if (x0 == 0) {
-        if (k0 != 2) aa_pull_xface<real, -1>(a, nb_x, x0, y, z, m0, p0);
-        if (n0 == 1 && k0 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0, y, z, m0, p0);
-        if (n0 == 2 && has1 && k1 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0 + 1, y, z, m1, p1);
+        if (k0 != 2) aa_pull_xface<real, -1>(a, nb_x, x0, y, z, p0);
+        if (n0 == 1 && k0 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0, y, z, p0);
+        if (n0 == 2 && has1 && k1 != 2) aa_pull_xface<real, 1>(a, direct_ptr(a, patch, 9), x0 + 1, y, z, p1);
     } else {
-        if (x0 == n0 - 1 && k0 != 2) aa_pull_xface<real, 1>(a, nb_x, x0, y, z, m0, p0);
-        if (has1 && x0 + 1 == n0 - 1 && k1 != 2) aa_pull_xface<real, 1>(a, nb_x, x0 + 1, y, z, m1, p1);
+        if (x0 == n0 - 1 && k0 != 2) aa_pull_xface<real, 1>(a, nb_x, x0, y, z, p0);
+        if (has1 && x0 + 1 == n0 - 1 && k1 != 2) aa_pull_xface<real, 1>(a, nb_x, x0 + 1, y, z, p1);
     }
 }
 
+// As the two-grid sweep, the AA kernels carry no wall logic: PULL scatters every
+// out_i to x + e_i, a wall cell included, and the bounce-back list's PULL fix-up
+// (aux_kernels.cu bb_list_kernel, mode 2) then moves out_i + corr from the wall's
+// slot i into A[x][opp(i)]; after LOCAL, its store-side mode (1) parks
+// out_j + corr in the wall slots A[x + e_j][j] that the next PULL gathers.  The
+// only reader of a wall slot written by the blind scatter is the fix-up, and
+// the only reader of A[x][opp(i)] is x's next LOCAL.  Only tiles holding a
+// non-fluid cell read the cells' kinds.
 template <typename real, bool PULL, int MINB, bool DIRECT>
 __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const SweepArgs<real> a)
 {
@@ -129,34 +135,35 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     const int x0 = pc.x0, y = pc.y, z = pc.z;
     const bool has1 = x0 + 1 < pc.xend;
     const Geom &g = a.g;
-    const int64_t qs = g.qs;
     const int64_t c = main_index(g, x0, y, z);
-    const int64_t fc = (int64_t)pc.patch * g.fs + flag_index(g, x0, y, z);
-    const uchar2 kk = *reinterpret_cast<const uchar2 *>(a.kind + fc);
-    const uint8_t k0 = kk.x, k1 = has1 ? kk.y : (uint8_t)2;
+    uint8_t k0 = 0, k1 = has1 ? 0 : 2;  // 2: non-fluid (or the phantom partner of an odd row end)
+    if (pc.solid) {
+        const uchar2 kk =
+            *reinterpret_cast<const uchar2 *>(a.kind + (int64_t)pc.patch * g.fs + flag_index(g, x0, y, z));
+        k0 = kk.x;
+        if (has1) k1 = kk.y;
+    }
     real *nb_x = nullptr;  // x-face neighbour for the direct ghost stores, loaded with the PDFs
     if (DIRECT && (x0 == 0 || x0 + 1 >= g.n[0] - 1)) nb_x = direct_ptr(a, pc.patch, x0 == 0 ? 8 : 9);
     real *P = a.dst + (int64_t)pc.patch * g.ps;  // in place
     real *A = P + c;
     real p0[Q], p1[Q];
     if (PULL) {
-        pull_pair<real>(a.off, A, ghost_base(g, (const real *)P, y, z), x0 == 0, x0 + 1 == g.n[0],
+        pull_pair<real>(a.off, a.chk, A, ghost_base(g, (const real *)P, y, z), x0 == 0, x0 + 1 == g.n[0],
                         x0 + 2 == g.n[0], p0, p1);
     } else {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
-            const V2 v = __ldg(at<const V2>(A, a.off.slot[i]));
+            const V2 v = gld(a.chk, at<const V2>(A, a.off.slot[i]));
             p0[i] = v.x;
             p1[i] = v.y;
         }
     }
     if (k0 == 2 && k1 == 2) return;
-    const uint32_t m0 = k0 == 1 ? a.wmask[fc] : 0u;
-    const uint32_t m1 = k1 == 1 ? a.wmask[fc + 1] : 0u;
     collide_pair(p0, p1, a.omega);
-    if (k0 == 0 && k1 == 0) {
-        // no wall next to either cell (the common case)
-        if (PULL) {
+    const bool both = k0 != 2 && k1 != 2;
+    if (PULL) {
+        if (both) {
             // straight-line scatter to x + e_i; a row-end target lives in the
             // x-ghost column, stored in a branch only warps holding a row end take
             const bool lo0 = x0 == 0, hi1 = x0 + 2 == g.n[0];
@@ -167,13 +174,13 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
                     V2 w;
                     w.x = p0[i];
                     w.y = p1[i];
-                    *reinterpret_cast<V2 *>(t) = w;
+                    gst(a.chk, reinterpret_cast<V2 *>(t), w);
                 } else if (EX(i) > 0) {  // to x + 1
-                    t[0] = p0[i];
-                    if (!hi1) t[1] = p1[i];
+                    gst(a.chk, t, p0[i]);
+                    if (!hi1) gst(a.chk, t + 1, p1[i]);
                 } else {  // to x - 1
-                    if (!lo0) t[0] = p0[i];
-                    t[1] = p1[i];
+                    if (!lo0) gst(a.chk, t, p0[i]);
+                    gst(a.chk, t + 1, p1[i]);
                 }
             }
             if (lo0 || hi1) {
@@ -182,95 +189,34 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
                 for (int i = 0; i < Q; ++i) {
                     if (EX(i) == 0) continue;
                     real *gt = at<real>(G, a.off.gpush[i]);
-                    if (EX(i) > 0 && hi1) *gt = p1[i];
-                    if (EX(i) < 0 && lo0) *gt = p0[i];
+                    if (EX(i) > 0 && hi1) gst(a.chk, gt, p1[i]);
+                    if (EX(i) < 0 && lo0) gst(a.chk, gt, p0[i]);
                 }
             }
         } else {
+            // one cell of the pair is non-fluid (or the phantom of an odd row end)
 #pragma unroll
             for (int i = 0; i < Q; ++i) {
-                V2 w;
-                w.x = p0[i];
-                w.y = p1[i];
-                *at<V2>(A, a.off.slot[OPP(i)]) = w;
+                if (k0 != 2) gst(a.chk, P + pdf_index(g, i, x0 + EX(i), y + EY(i), z + EZ(i)), p0[i]);
+                if (k1 != 2) gst(a.chk, P + pdf_index(g, i, x0 + 1 + EX(i), y + EY(i), z + EZ(i)), p1[i]);
             }
+        }
+    } else if (both) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+            V2 w;
+            w.x = p0[i];
+            w.y = p1[i];
+            gst(a.chk, at<V2>(A, a.off.oslot[i]), w);
         }
     } else {
-        // a non-fluid cell in the pair or a wall next to one: coordinates are
-        // recomputed here rather than kept live through the collision
-        const PairCoord q = locate_pair(a);
-        const int qx = q.x0, qy = q.y, qz = q.z;
-        const int64_t fq = (int64_t)q.patch * g.fs + flag_index(g, qx, qy, qz);
-        real *Pq = a.dst + (int64_t)q.patch * g.ps;
-        real *Aq = Pq + main_index(g, qx, qy, qz);
-        const bool both = k0 != 2 && k1 != 2;
-        if (PULL) {
 #pragma unroll
-            for (int i = 0; i < Q; ++i) {
-                const bool r0 = (m0 >> i) & 1u, r1 = (m1 >> i) & 1u;  // x + e_i is a wall: bounce back into x
-                if (EX(i) == 0 && both && !r0 && !r1) {
-                    V2 w;
-                    w.x = p0[i];
-                    w.y = p1[i];
-                    *reinterpret_cast<V2 *>(Aq + i * qs + yz_shift(g, i)) = w;
-                    continue;
-                }
-                if (k0 != 2) {
-                    if (r0) {
-                        real v = p0[i];
-                        const uint8_t f = a.flags[fq + flag_shift(g, i)];
-                        if (f >= 2) v += a.corr[(f - 2) * Q + OPP(i)];
-                        Aq[OPP(i) * qs] = v;
-                    } else {
-                        Pq[pdf_index(g, i, qx + EX(i), qy + EY(i), qz + EZ(i))] = p0[i];
-                    }
-                }
-                if (k1 != 2) {
-                    if (r1) {
-                        real v = p1[i];
-                        const uint8_t f = a.flags[fq + 1 + flag_shift(g, i)];
-                        if (f >= 2) v += a.corr[(f - 2) * Q + OPP(i)];
-                        Aq[OPP(i) * qs + 1] = v;
-                    } else {
-                        Pq[pdf_index(g, i, qx + 1 + EX(i), qy + EY(i), qz + EZ(i))] = p1[i];
-                    }
-                }
-            }
-        } else {
-            if (both) {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    V2 w;
-                    w.x = p0[i];
-                    w.y = p1[i];
-                    *reinterpret_cast<V2 *>(Aq + OPP(i) * qs) = w;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    if (k0 != 2) Aq[OPP(i) * qs] = p0[i];
-                    if (k1 != 2) Aq[OPP(i) * qs + 1] = p1[i];
-                }
-            }
-            // store-side bounce-back into wall slots: A[x + e_j][j] = out_j + corr
-#pragma unroll
-            for (int j = 1; j < Q; ++j) {
-                if ((m0 >> j) & 1u) {
-                    real v = p0[j];
-                    const uint8_t f = a.flags[fq + flag_shift(g, j)];
-                    if (f >= 2) v += a.corr[(f - 2) * Q + OPP(j)];
-                    Pq[pdf_index(g, j, qx + EX(j), qy + EY(j), qz + EZ(j))] = v;
-                }
-                if ((m1 >> j) & 1u) {
-                    real v = p1[j];
-                    const uint8_t f = a.flags[fq + 1 + flag_shift(g, j)];
-                    if (f >= 2) v += a.corr[(f - 2) * Q + OPP(j)];
-                    Pq[pdf_index(g, j, qx + 1 + EX(j), qy + EY(j), qz + EZ(j))] = v;
-                }
-            }
+        for (int i = 0; i < Q; ++i) {
+            if (k0 != 2) gst(a.chk, at<real>(A, a.off.oslot[i]), p0[i]);
+            if (k1 != 2) gst(a.chk, at<real>(A, a.off.oslot[i]) + 1, p1[i]);
         }
     }
-    if (DIRECT) aa_direct_pair<real, PULL>(a, pc.patch, x0, y, z, has1, k0, k1, m0, m1, p0, p1, nb_x);
+    if (DIRECT) aa_direct_pair<real, PULL>(a, pc.patch, x0, y, z, has1, k0, k1, p0, p1, nb_x);
 }
 
 template <typename real>

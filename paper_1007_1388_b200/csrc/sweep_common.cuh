@@ -61,6 +61,55 @@ __device__ __forceinline__ real *ghost_base(const Geom &g, real *P, int y, int z
     return P + g.gbase + (int64_t)(z + 1) * g.gy + (y + g.gyo);
 }
 
+// Global loads / stores of PDF values (kernels.cuh Checker): plain __ldg / store
+// in the product build, checked and recorded in the checked build.
+__device__ __forceinline__ void ck_access(const Checker &c, const void *p, int bytes, bool write)
+{
+#ifdef LBM_CHECKED
+    const char *cp = static_cast<const char *>(p);
+    int gi = -1;
+    for (int k = 0; k < 2; ++k)
+        if (c.lo[k] && cp >= c.lo[k] && cp + bytes <= c.hi[k]) gi = k;
+    if (gi < 0 || ((uintptr_t)cp % (uintptr_t)bytes) != 0) {
+        atomicAdd(c.err + 0, 1ull);
+        return;
+    }
+    const int64_t e0 = (int64_t)((cp - c.lo[gi]) / c.esize);
+    const unsigned long long tid =
+        (unsigned long long)blockIdx.x * blockDim.x * blockDim.y + threadIdx.y * blockDim.x + threadIdx.x + 1;
+    const unsigned long long id = c.launch | tid;
+    for (int k = 0; k < bytes / c.esize; ++k) {
+        const int64_t e = gi * c.elems + e0 + k;
+        if (write) {
+            if (atomicExch(c.wr + e, id) != 0ull) atomicAdd(c.err + 1, 1ull);
+            const unsigned long long r = atomicAdd(c.rd + e, 0ull);
+            if (r != 0ull && (r >> 32) == (id >> 32) && r != id) atomicAdd(c.err + 2, 1ull);
+        } else {
+            atomicExch(c.rd + e, id);
+            const unsigned long long w = atomicAdd(c.wr + e, 0ull);
+            if (w != 0ull && (w >> 32) == (id >> 32) && w != id) atomicAdd(c.err + 2, 1ull);
+        }
+    }
+#else
+    (void)c;
+    (void)p;
+    (void)bytes;
+    (void)write;
+#endif
+}
+template <typename T>
+__device__ __forceinline__ T gld(const Checker &c, const T *p)
+{
+    ck_access(c, p, (int)sizeof(T), false);
+    return __ldg(p);
+}
+template <typename T>
+__device__ __forceinline__ void gst(const Checker &c, T *p, const T &v)
+{
+    ck_access(c, p, (int)sizeof(T), true);
+    *p = v;
+}
+
 // two cells per thread along x: the 2-vector type of the storage precision
 template <typename real> struct Vec2;
 template <> struct Vec2<float> { using T = float2; };

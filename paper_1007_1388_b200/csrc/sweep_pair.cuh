@@ -24,25 +24,25 @@ namespace lbm {
 // before any is consumed.  The phantom partner of an odd row end reads in-bounds
 // garbage that is never used.
 template <typename real>
-__device__ __forceinline__ void pull_pair(const DirOffsets &o, const real *C, const real *G, bool lo0, bool hi0,
-                                          bool hi1, real (&p0)[Q], real (&p1)[Q])
+__device__ __forceinline__ void pull_pair(const DirOffsets &o, const Checker &ck, const real *C, const real *G,
+                                          bool lo0, bool hi0, bool hi1, real (&p0)[Q], real (&p1)[Q])
 {
     using V2 = typename Vec2<real>::T;
 #pragma unroll
     for (int i = 0; i < Q; ++i) {
         const real *s = at<const real>(C, o.pull[i]);
         if (EX(i) == 0) {
-            const V2 v = __ldg(reinterpret_cast<const V2 *>(s));
+            const V2 v = gld(ck, reinterpret_cast<const V2 *>(s));
             p0[i] = v.x;
             p1[i] = v.y;
         } else {
             const real *gs = at<const real>(G, o.gpull[i]);
             if (EX(i) > 0) {
-                p0[i] = __ldg(lo0 ? gs : s);
-                p1[i] = __ldg(s + 1);
+                p0[i] = gld(ck, lo0 ? gs : s);
+                p1[i] = gld(ck, s + 1);
             } else {
-                p0[i] = __ldg(hi0 ? gs : s);
-                p1[i] = __ldg(hi1 ? gs : s + 1);
+                p0[i] = gld(ck, hi0 ? gs : s);
+                p1[i] = gld(ck, hi1 ? gs : s + 1);
             }
         }
     }

@@ -24,6 +24,9 @@ STATUS = {0: "LBM_OK", 1: "LBM_ERR_ARG", 2: "LBM_ERR_STATE", 3: "LBM_ERR_OOM", 4
           5: "LBM_ERR_NCCL", 6: "LBM_ERR_INTERNAL"}
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblbm_b200.so")
+# LBM_LIBRARY selects another build of the same ABI -- the checked build
+# (liblbm_b200_checked.so, tools/sanitize_cases.py); there is no fallback.
+LIB_PATH = os.environ.get("LBM_LIBRARY") or LIB_PATH
 
 # Every symbol include/lbm.h declares (checked by tests/test_abi.py).
 EXPORTED = ("lbm_abi_version", "lbm_config_default", "lbm_create", "lbm_create_ex", "lbm_destroy",

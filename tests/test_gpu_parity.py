@@ -424,3 +424,63 @@ def test_flags_upload_complete_at_size():
             with m.Lattice(n, n, inputs.LDC_OMEGA, prec) as L:
                 L.set_flags(fl, wu)
                 np.testing.assert_array_equal(L.get_flags(), fl)
+
+
+# ---------------------------------------------------------------- walls outside the sweep
+# The sweeps carry no wall logic: the bounce-back list kernel (store side after a
+# two-grid sweep / AA LOCAL, fix-up after AA PULL) handles every wall link, each
+# entry carrying its wall mask and the shared velocity of its moving walls; tiles
+# holding a non-fluid cell read the cells' kinds (per-tile descriptor bit).
+
+def _mixed_wall_geometry(n):
+    """A cavity whose fluid cells touch walls of three velocities at once: the lid
+    (velocity 0), a moving-wall slab of velocity 1 just under it along y = 0, and a
+    no-slip post, so some cells' moving walls disagree (the list entry's mixed case
+    reads each wall's flag) while others share one velocity."""
+    fl, wu = inputs.ldc_flags(n)
+    nx, ny, nz = n
+    fl[nz, 1, 1:nx + 1] = inputs.VELOCITY0 + 1       # z = nz - 1, y = 0: a second moving wall under the lid
+    fl[1:nz + 1, ny // 2, nx // 2] = inputs.NOSLIP    # a no-slip post through the cavity
+    fl[nz - 2, 3:6, 5:9] = inputs.VELOCITY0 + 2       # a moving block near the lid (velocity 2)
+    wu = np.vstack([wu, [[0.0, 0.03, -0.01]], [[-0.02, 0.0, 0.015]]])
+    return fl, wu
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_mixed_moving_walls_vs_oracle(prec, layout):
+    n = (70, 23, 17)  # two x tiles (the second ragged), ragged y
+    fl, wu = _mixed_wall_geometry(n)
+    f0 = inputs.noise_pdfs(n, seed=29)
+    ref = oracle.run(f0, fl, wu, 1.1, 25, nthreads=oracle.max_threads())
+    got = run_gpu(n, fl, wu, f0, 25, prec, omega=1.1, patch=(70, 23, 17) if layout == 0 else (35, 23, 17),
+                  layout=layout)
+    assert max_fluid_diff(got, ref, fl) <= TOL[prec]
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+def test_set_flags_again_rebuilds_wall_lists(layout):
+    """set_flags after steps replaces the bounce-back list and the tiles' non-fluid
+    bits: a run that starts from obstacles A, steps, switches to obstacles B and
+    steps on matches the oracle run that does the same from B's switch point."""
+    n = (48, 20, 14)
+    fa, wu = inputs.ldc_flags(n)
+    fa = inputs.add_obstacles(fa, 0.06, seed=41, kinds=(inputs.NOSLIP,))
+    fb, _ = inputs.ldc_flags(n)
+    fb = inputs.add_obstacles(fb, 0.05, seed=43, kinds=(inputs.NOSLIP, inputs.VELOCITY0 + 1))
+    wub = np.vstack([wu, [[0.01, 0.0, 0.02]]])
+    f0 = inputs.noise_pdfs(n, seed=47)
+    L = lbm().Lattice(n, (24, 20, 14), 1.4, 8, layout=layout)
+    try:
+        L.set_flags(fa, wu)
+        L.set_pdfs(f0)
+        L.step(8)  # even: the AA layout accepts set_flags only in its swapped phase
+        mid = L.get_pdfs()
+        L.set_flags(fb, wub)
+        L.set_pdfs(mid)  # cells fluid in B but solid in A start from zero
+        L.step(9)
+        got = L.get_pdfs()
+    finally:
+        L.close()
+    ref = oracle.run(mid, fb, wub, 1.4, 9, nthreads=oracle.max_threads())
+    assert max_fluid_diff(got, ref, fb) <= TOL[8]

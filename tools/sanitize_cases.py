@@ -1,11 +1,16 @@
-"""Small cases for compute-sanitizer (memcheck / racecheck / initcheck /
-synccheck): every sweep family and exchange path once, in both precisions --
-two grids and AA, both occupancy variants, multi-patch direct ghost stores,
-the NCCL exchange with the shell / interior overlap (FORCE_BUFFERS, one-rank
-communicator) and the fused exchange with its epoch handshake (SELF_PEER),
-with periodic wrap, obstacles on patch faces and two moving walls.
+"""Small cases covering every sweep family and exchange path once, in both
+precisions -- two grids and AA, both occupancy variants, multi-patch direct
+ghost stores, the NCCL exchange with the shell / interior overlap
+(FORCE_BUFFERS, one-rank communicator) and the fused exchange with its epoch
+handshake (SELF_PEER), with periodic wrap, obstacles on patch faces and two
+moving walls.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_cases.py
+compute-sanitizer is closed on the GPU pool (its runs left GPUs needing a
+reset), so the cases run against the checked build instead (make checked;
+kernels.cuh Checker: bounds, single writer per step, read/write races within
+a launch), which fails the step with LBM_ERR_INTERNAL on any finding:
+
+    LBM_LIBRARY=paper_1007_1388_b200/liblbm_b200_checked.so python tools/sanitize_cases.py
 """
 import os
 import sys
@@ -37,6 +42,10 @@ def run(layout=0, prec=8, env=None, exchange_mode=0, n=(36, 21, 13), patches=((3
 
 
 if __name__ == "__main__":
+    if "--first" in sys.argv:  # one case (the checked build's negative control)
+        run(0, 8, patches=((36, 21, 13),))
+        print("first case done")
+        sys.exit(0)
     for prec in (8, 4):
         for layout in (0, 1):
             run(layout, prec)                                         # one patch, several, direct stores

@@ -16,10 +16,11 @@ LIB = os.path.join(ROOT, "paper_1007_1388_b200", "liblbm_b200.so")
 # the default launch configurations (sweep.cu / sweep_aa.cu launch wrappers, variant 0)
 KERNELS = {
     "sweep_x2_fp64": "_ZN3lbm15sweep_x2_kernelIdLi3ELb0EEEvNS_9SweepArgsIT_EE",
-    "sweep_x2_fp32": "_ZN3lbm15sweep_x2_kernelIfLi4ELb0EEEvNS_9SweepArgsIT_EE",
-    "sweep_x2_direct_fp32": "_ZN3lbm15sweep_x2_kernelIfLi4ELb1EEEvNS_9SweepArgsIT_EE",
+    "sweep_x2_fp32": "_ZN3lbm15sweep_x2_kernelIfLi5ELb0EEEvNS_9SweepArgsIT_EE",
+    "sweep_x2_direct_fp32": "_ZN3lbm15sweep_x2_kernelIfLi5ELb1EEEvNS_9SweepArgsIT_EE",
     "sweep_aa_pull_fp64": "_ZN3lbm18sweep_aa_x2_kernelIdLb1ELi3ELb0EEEvNS_9SweepArgsIT_EE",
     "sweep_aa_local_fp64": "_ZN3lbm18sweep_aa_x2_kernelIdLb0ELi3ELb0EEEvNS_9SweepArgsIT_EE",
+    "bb_list_fp64_mode0": "_ZN3lbm14bb_list_kernelIdLi0EEEvPT_PKhPKNS_7BbEntryElPKS1_NS_4GeomENS_7CheckerE",
 }
 
 
@@ -41,7 +42,7 @@ def mix(lines):
         base = op.split(".")[0]
         if base in ("LDG", "STG", "LDL", "STL", "LDS", "STS"):
             c[op] += 1
-        elif base in ("DFMA", "DADD", "DMUL", "FFMA", "FADD", "FMUL", "BRA", "EXIT", "UTMALDG", "SEL"):
+        elif base in ("DFMA", "DADD", "DMUL", "FFMA", "FADD", "FMUL", "FFMA2", "FADD2", "FMUL2", "BRA", "EXIT", "SEL", "IMAD", "IADD3", "LEA"):
             c[base] += 1
         c["total"] += 1
     return c
