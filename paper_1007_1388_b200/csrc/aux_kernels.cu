@@ -436,17 +436,18 @@ cudaError_t launch_gather(const real *grid, const uint8_t *flags, const int64_t 
 // The sweeps themselves carry no wall logic.  Each target slot has exactly one
 // writer (x = w - e_j), so entries are independent.
 template <typename real, int mode>
-__global__ void __launch_bounds__(256, 3) bb_list_kernel(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n,
-                                                      const real *corr, const Geom g, const Checker ck)
+__global__ void __launch_bounds__(256) bb_list_kernel(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n,
+                                                      const real *corr, const Geom g, const BbOffsets o,
+                                                      const Checker ck)
 {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const BbEntry en = list[t];
-        const int64_t lp = (int64_t)(en.idx / (uint64_t)g.fs);
-        const int64_t e = (int64_t)(en.idx - (uint64_t)lp * (uint64_t)g.fs);
-        real *gp = grid + lp * g.ps;
-        const int x = (int)(e % g.fpx) - g.fxo;
-        const int64_t r = e / g.fpx;
-        const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
+        const int lp = (int)(en.pos >> 45);
+        const int z = (int)((en.pos >> 30) & 0x7fff), y = (int)((en.pos >> 15) & 0x7fff), x = (int)(en.pos & 0x7fff);
+        real *gp = grid + (int64_t)lp * g.ps;
+        real *C = gp + main_index(g, x, y, z);
+        real *G = ghost_base(g, gp, y, z);
+        const bool xlo = x == 0, xhi = x == g.n[0] - 1;
         const uint32_t vel = en.vinfo >> 24;
         // all link values first, then the stores: no slot is both read and
         // written by this kernel (reads: fluid slots in modes 0 / 1, wall slots in
@@ -456,23 +457,24 @@ __global__ void __launch_bounds__(256, 3) bb_list_kernel(real *grid, const uint8
 #pragma unroll
         for (int j = 1; j < Q; ++j) {
             if (!((en.mask >> j) & 1u)) continue;
-            const int64_t src = mode == 2 ? pdf_index(g, j, x + EX(j), y + EY(j), z + EZ(j))
-                                          : pdf_index(g, mode == 1 ? OPP(j) : j, x, y, z);
-            v[j] = gld(ck, gp + src);
+            const bool cross = (EX(j) < 0 && xlo) || (EX(j) > 0 && xhi);  // w is an x ghost
+            const real *src = mode == 2 ? (cross ? at<real>(G, o.wg[j]) : at<real>(C, o.wm[j])) : at<real>(C, o.xs[j]);
+            v[j] = gld(ck, src);
+            if ((en.vinfo >> j) & 1u) {  // moving wall: its velocity is shared (vel) or read from its flag
+                const int k = vel != kBbMixed
+                                  ? (int)vel
+                                  : __ldg(flags + (int64_t)lp * g.fs + flag_index(g, x + EX(j), y + EY(j), z + EZ(j))) - 2;
+                v[j] += __ldg(corr + k * Q + OPP(j));
+            }
         }
 #pragma unroll
         for (int j = 1; j < Q; ++j) {
             if (!((en.mask >> j) & 1u)) continue;
-            const int64_t dst = mode == 2 ? pdf_index(g, OPP(j), x, y, z)
-                                          : pdf_index(g, mode == 1 ? j : OPP(j), x + EX(j), y + EY(j), z + EZ(j));
-            real w = v[j];
-            if ((en.vinfo >> j) & 1u) {  // moving wall: its velocity is shared (vel) or read from its flag
-                const int k = vel != kBbMixed ? (int)vel : flags[lp * g.fs + e + flag_shift(g, j)] - 2;
-                w += corr[k * Q + OPP(j)];
-            }
-            gst(ck, gp + dst, w);
+            const bool cross = (EX(j) < 0 && xlo) || (EX(j) > 0 && xhi);
+            real *dst = mode == 2 ? at<real>(C, o.xs[j]) : (cross ? at<real>(G, o.wg[j]) : at<real>(C, o.wm[j]));
+            gst(ck, dst, v[j]);
 #ifdef LBM_CHECKED
-            if (ck.inject) gst(ck, gp + dst, w);
+            if (ck.inject) gst(ck, dst, v[j]);
 #endif
         }
     }
@@ -480,13 +482,13 @@ __global__ void __launch_bounds__(256, 3) bb_list_kernel(real *grid, const uint8
 
 template <typename real>
 cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n, const real *corr,
-                           const Geom &g, int mode, const Checker &ck, cudaStream_t s)
+                           const Geom &g, int mode, const BbOffsets &o, const Checker &ck, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
-    if (mode == 2) bb_list_kernel<real, 2><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
-    else if (mode == 1) bb_list_kernel<real, 1><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
-    else bb_list_kernel<real, 0><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, ck);
+    if (mode == 2) bb_list_kernel<real, 2><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, o, ck);
+    else if (mode == 1) bb_list_kernel<real, 1><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, o, ck);
+    else bb_list_kernel<real, 0><<<(unsigned)blocks, 256, 0, s>>>(grid, flags, list, n, corr, g, o, ck);
     return cudaGetLastError();
 }
 
@@ -529,7 +531,9 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask,
         const int64_t i = base + k;
         if (i >= total || kind[i] != 1) continue;
         BbEntry en;
-        en.idx = (uint64_t)i;
+        const int64_t lp = i / g.fs, e = i - lp * g.fs;
+        const int64_t r = e / g.fpx;
+        en.pos = bb_pos((int)lp, (int)(e % g.fpx) - g.fxo, (int)(r % g.py) - 1, (int)(r / g.py) - 1);
         en.mask = wmask[i];
         uint32_t vm = 0, vel = kBbMixed + 1;  // kBbMixed + 1: no moving wall yet
         for (int j = 1; j < Q; ++j) {
@@ -597,7 +601,8 @@ cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const
                                                     const real *, real *, const uint8_t *, const Geom &,       \
                                                     cudaStream_t);                                             \
     template cudaError_t launch_bb_list<real>(real *, const uint8_t *, const BbEntry *, int64_t, const real *,  \
-                                              const Geom &, int, const Checker &, cudaStream_t);               \
+                                              const Geom &, int, const BbOffsets &, const Checker &,           \
+                                              cudaStream_t);                                                   \
     template cudaError_t launch_import<real>(const double *, int64_t, int64_t, const int64_t *, const int64_t *, \
                                              const int *, const Geom &, real *, int, cudaStream_t);            \
     template cudaError_t launch_export<real>(const real *, const uint8_t *, int64_t, int64_t, const int64_t *,  \

@@ -127,18 +127,31 @@ cudaError_t launch_copy_segments(const CopySeg *segs, int nseg, int64_t max_elem
 // Half-way bounce-back over the list of wall-adjacent fluid cells (modes in
 // aux_kernels.cu bb_list_kernel: 0 two-grid store side, 1 AA LOCAL store side /
 // swapped state, 2 AA PULL fix-up), after every sweep and once after the state
-// or the flags are set.  One entry per cell: its flag-layout index
-// (patch * fs + e, ascending), wall mask (bit j: x + e_j is non-fluid) and
+// or the flags are set.  One entry per cell, in ascending memory order: its
+// position, wall mask (bit j: x + e_j is non-fluid) and
 // vinfo = bits j of the moving walls | their shared velocity index << 24
 // (kBbMixed: the walls move differently -- read each wall's flag).
 struct BbEntry {
-    uint64_t idx;
+    uint64_t pos;  // patch << 45 | z << 30 | y << 15 | x (bb_pos)
     uint32_t mask, vinfo;
 };
+__host__ __device__ constexpr uint64_t bb_pos(int patch, int x, int y, int z)
+{
+    return (uint64_t)patch << 45 | (uint64_t)z << 30 | (uint64_t)y << 15 | (uint64_t)x;
+}
+// Byte offsets of a wall link x -> w = x + e_j in the bounce-back list kernel,
+// uniform over a launch (filled on the host per mode, fill_bb_offsets): xs[j]
+// the slot of x it reads or writes (relative to x's element in slice 0), wm[j]
+// the slot of w when w lies in the main slices (same base), wg[j] when w is an
+// x ghost (relative to x's ghost-column base, ghost_base).
+struct BbOffsets {
+    int64_t xs[Q], wm[Q], wg[Q];
+};
+void fill_bb_offsets(const Geom &g, int mode, int esize, BbOffsets &o);
 constexpr uint32_t kBbMixed = 255;
 template <typename real>
 cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list, int64_t n, const real *corr,
-                           const Geom &g, int mode, const Checker &ck, cudaStream_t s);
+                           const Geom &g, int mode, const BbOffsets &o, const Checker &ck, cudaStream_t s);
 // Building the list (kind == 1 cells of all `total` flag-layout elements): per-chunk
 // counts (bb_list_chunks(total) of them), then, with their exclusive scan, the entries.
 int64_t bb_list_chunks(int64_t total);

@@ -205,14 +205,26 @@ lbm_status exchange_seq(lbm_ctx *ctx, int gi, cudaStream_t s, TimingSlot *ts, in
     return LBM_OK;
 }
 
+void fill_bb_offsets(const Geom &g, int mode, int esize, BbOffsets &o)
+{
+    for (int j = 0; j < Q; ++j) {
+        const int xslot = mode == 0 ? j : OPPf(j), wslot = mode == 0 ? OPPf(j) : j;
+        o.xs[j] = xslot * g.qs * esize;
+        o.wm[j] = (wslot * g.qs + EXf(j) + EYf(j) * (int64_t)g.px + EZf(j) * g.plane) * esize;
+        o.wg[j] = (wslot * g.gq + (EXf(j) < 0 ? 0 : g.gside) + EYf(j) + EZf(j) * (int64_t)g.gy) * esize;
+    }
+}
+
 lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s)
 {
     if (ctx->bb_n == 0) return LBM_OK;
+    BbOffsets o;
+    fill_bb_offsets(ctx->g, mode, ctx->esize, o);
     cudaError_t e = ctx->esize == 8
                         ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
-                                                 (const double *)ctx->corr, ctx->g, mode, next_checker(ctx), s)
+                                                 (const double *)ctx->corr, ctx->g, mode, o, next_checker(ctx), s)
                         : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
-                                                (const float *)ctx->corr, ctx->g, mode, next_checker(ctx), s);
+                                                (const float *)ctx->corr, ctx->g, mode, o, next_checker(ctx), s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "bounce-back list launch", __FILE__, __LINE__);
     ctx->launches += 1;
     return LBM_OK;
