@@ -116,6 +116,8 @@ const char *decompose(const lbm_config &cfg, Decomp &dec)
     // segments (peer = this rank)
     dec.force_buffers = cfg.exchange_mode != LBM_EXCHANGE_AUTO;
     dec.nlocal = dec.brick[0] * dec.brick[1] * dec.brick[2];
+    // the bounce-back list packs a cell's patch into 19 bits (kernels.cuh bb_pos)
+    if (dec.nlocal >= (1 << 19)) return "too many patches per rank (at most 524287)";
     for (int a = 0; a < 3; ++a) {
         dec.owned_lo[a] = (int64_t)dec.coord[a] * dec.brick[a] * dec.patch[a];
         dec.owned_hi[a] = dec.owned_lo[a] + (int64_t)dec.brick[a] * dec.patch[a];

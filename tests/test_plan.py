@@ -96,6 +96,9 @@ def test_decomposition_defaults():
         assert tuple(info["proc_grid"]) == grid
     with pytest.raises(lbm.LbmError):
         lbm.plan(lbm.default_config((16, 16, 16), (16, 16, 16), nranks=2))  # 1 patch, 2 ranks
+    # the bounce-back list packs a cell's patch into 19 bits: at most 2^19 - 1 patches per rank
+    with pytest.raises(lbm.LbmError, match="too many patches per rank"):
+        lbm.plan(lbm.default_config((128, 64, 64), (1, 1, 1)))
 
 
 # ----------------------------------------------------------------------------- emulation
