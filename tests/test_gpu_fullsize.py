@@ -57,22 +57,32 @@ def test_full_size_sampled_planes(n, prec, patch, layout):
         L.close()
 
 
-@pytest.mark.parametrize("prec", [8, 4])
-def test_ldc256_100_steps_every_cell_vs_oracle(prec):
-    """SURVEY 8(d) row 2: BASELINE configs[1] (LDC 256^3 fp64 and fp32, dyadic
-    noise start, the bench's launch path) after 100 steps, every PDF of every
-    fluid cell against the OpenMP oracle (~20 s on the host cores): <= 1e-12
-    (fp64), <= 1e-5 (fp32)."""
-    from paper_1007_1388_b200 import lbm
+@pytest.fixture(scope="module")
+def ldc256_ref():
+    """The oracle's LDC 256^3 state after 100 steps from the dyadic-noise start
+    (~20 s on the host cores), shared by the precision / layout cases."""
     n = (256, 256, 256)
     fl, wu = inputs.ldc_flags(n)
     f0 = inputs.noise_pdfs(n)
-    with lbm.Lattice(n, n, inputs.LDC_OMEGA, prec, device=0) as L:
+    return fl, wu, oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 100, nthreads=oracle.max_threads())
+
+
+@pytest.mark.parametrize("prec,layout", [(8, "ab"), (4, "ab"), (8, "aa"), (4, "aa")])
+def test_ldc256_100_steps_every_cell_vs_oracle(prec, layout, ldc256_ref):
+    """SURVEY 8(d) row 2: BASELINE configs[1] (LDC 256^3 fp64 and fp32, dyadic
+    noise start, the bench's launch path: graph pairs, the bounce-back list after
+    every sweep) after 100 steps, every PDF of every fluid cell against the OpenMP
+    oracle: <= 1e-12 (fp64), <= 1e-5 (fp32); two grids and the AA layout (blind
+    PULL scatter + the list's fix-up)."""
+    from paper_1007_1388_b200 import lbm
+    n = (256, 256, 256)
+    fl, wu, ref = ldc256_ref
+    with lbm.Lattice(n, n, inputs.LDC_OMEGA, prec, device=0,
+                     layout=lbm.LBM_LAYOUT_AA if layout == "aa" else lbm.LBM_LAYOUT_AB) as L:
         L.set_flags(fl, wu)
-        L.init_noise(inputs.NOISE_SEED)  # the same state as f0, generated on the device
+        L.init_noise(inputs.NOISE_SEED)  # the same state as the oracle's start, generated on the device
         L.step(100)
         got = L.get_pdfs()
-    ref = oracle.run(f0, fl, wu, inputs.LDC_OMEGA, 100, nthreads=oracle.max_threads())
     mask = fl[1:-1, 1:-1, 1:-1] == 0
     err = float(np.abs(got[mask] - ref[mask]).max())
     assert err <= (1e-12 if prec == 8 else 1e-5), err
