@@ -499,14 +499,36 @@ cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list
 // counts per chunk, the host scans the counts, pass 1 writes each chunk's
 // entries at its offset in order.
 constexpr int kBbChunk = 256 * 8;
-__global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
-                                     const Geom g, int64_t *counts, BbEntry *list)
+// The wall mask of list entry i (0: not an entry): kind-1 cells, minus the x
+// links of the inner face cells of uniform-wall sides, which the two-grid sweep
+// stores itself (xwall_kernel).
+__device__ __forceinline__ uint32_t bb_entry_mask(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall,
+                                                  const Geom &g, int64_t i)
+{
+    if (kind[i] != 1) return 0u;
+    uint32_t m = wmask[i];
+    if (xwall) {
+        const int64_t lp = i / g.fs, e = i - lp * g.fs;
+        const int x = (int)(e % g.fpx) - g.fxo;
+        const int64_t r = e / g.fpx;
+        const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
+        const uint32_t xw = xwall[lp];
+        const bool inner = y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2;
+        if ((xw & 1u) && inner && x == 0) m &= ~kXM;
+        if ((xw & 2u) && inner && x == g.n[0] - 1) m &= ~kXP;
+    }
+    return m;
+}
+
+__global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
+                                     const uint32_t *xwall, int64_t total, const Geom g, int64_t *counts,
+                                     BbEntry *list)
 {
     __shared__ int warp_tot[8];
     const int64_t base = (int64_t)blockIdx.x * kBbChunk + (int64_t)threadIdx.x * 8;
     int mine = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mine += (base + k < total && kind[base + k] == 1) ? 1 : 0;
+    for (int k = 0; k < 8; ++k) mine += (base + k < total && bb_entry_mask(kind, wmask, xwall, g, base + k)) ? 1 : 0;
     // block-exclusive scan of the per-thread counts (thread order = index order)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int incl = mine;
@@ -529,12 +551,13 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask,
     int64_t pos = counts[blockIdx.x] + before + incl - mine;
     for (int k = 0; k < 8; ++k) {
         const int64_t i = base + k;
-        if (i >= total || kind[i] != 1) continue;
+        const uint32_t m = i < total ? bb_entry_mask(kind, wmask, xwall, g, i) : 0u;
+        if (!m) continue;
         BbEntry en;
         const int64_t lp = i / g.fs, e = i - lp * g.fs;
         const int64_t r = e / g.fpx;
         en.pos = bb_pos((int)lp, (int)(e % g.fpx) - g.fxo, (int)(r % g.py) - 1, (int)(r / g.py) - 1);
-        en.mask = wmask[i];
+        en.mask = m;
         uint32_t vm = 0, vel = kBbMixed + 1;  // kBbMixed + 1: no moving wall yet
         for (int j = 1; j < Q; ++j) {
             if (!((en.mask >> j) & 1u)) continue;
@@ -549,50 +572,85 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask,
     }
 }
 
-cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s)
+cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall, int64_t total,
+                                 const Geom &g, int64_t *counts, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
     if (blocks > 0)
-        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, nullptr, nullptr, total, Geom{}, counts, nullptr);
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, nullptr, xwall, total, g, counts, nullptr);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
-                                 const Geom &g, const int64_t *offsets, BbEntry *list, cudaStream_t s)
+cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
+                                 const uint32_t *xwall, int64_t total, const Geom &g, const int64_t *offsets,
+                                 BbEntry *list, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
     if (blocks > 0)
-        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, flags, total, g, (int64_t *)offsets,
-                                                              list);
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, flags, xwall, total, g,
+                                                              (int64_t *)offsets, list);
     return cudaGetLastError();
 }
 
 int64_t bb_list_chunks(int64_t total) { return (total + kBbChunk - 1) / kBbChunk; }
 
-// Sweep tiles that hold a non-fluid cell: bit 31 of the descriptor's patch field
-// (sweep_common.cuh locate_pair).  Tiles without one -- every tile of a cavity
-// interior -- sweep without reading the per-cell kind.  One block per tile.
-__global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, const Geom g)
+// Tile bits (sweep_common.cuh locate_pair): bit 31 of the patch field, the tile
+// holds a non-fluid cell -- only those tiles read the cells' kinds; bits 30 / 29,
+// the patch's -x / +x side is a uniform wall (xwall) -- the two-grid sweep stores
+// the x links' bounce-back of that face's inner cells from its row-end lanes --
+// with the wall's flag in bits 16-23 / 24-31 of the z field.  One block per tile.
+__global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom g)
 {
     for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
         const int4 t = tiles[b];
-        const int patch = t.x & 0x7fffffff;
+        const int patch = t.x & 0x1fffffff, z = t.w & 0xffff;
         const int x0 = (int)((unsigned)t.y >> 16), xend = t.y & 0xffff;
         const int y0 = (int)((unsigned)t.z >> 16), yend = t.z & 0xffff;
         const int x = x0 + (int)(threadIdx.x % SWEEP_BX), y = y0 + (int)(threadIdx.x / SWEEP_BX);
-        const bool solid =
-            x < xend && y < yend && kind[(int64_t)patch * g.fs + flag_index(g, x, y, t.w)] == 2;
+        const bool solid = x < xend && y < yend && kind[(int64_t)patch * g.fs + flag_index(g, x, y, z)] == 2;
         const int any = __syncthreads_or(solid);
-        if (threadIdx.x == 0) tiles[b].x = patch | (any ? (int)0x80000000u : 0);
+        if (threadIdx.x == 0) {
+            const uint32_t xw = xwall ? xwall[patch] : 0u;
+            tiles[b].x = patch | (any ? (int)0x80000000u : 0) | (int)((xw & 1u) << 30) | (int)((xw & 2u) << 28);
+            tiles[b].w = z | (int)((xw & 0xffff00u) << 8);
+        }
         __syncthreads();
     }
 }
 
-cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const Geom &g, cudaStream_t s)
+// Per local patch, xwall = lo | hi << 1 | f_lo << 8 | f_hi << 16: a side is a
+// uniform wall (lo / hi) when every ghost cell its face's inner cells (y in
+// [1, n1 - 2], z in [1, n2 - 2]) link to -- the column part y in [0, n1 - 1],
+// z in [0, n2 - 1] -- carries one non-fluid flag f.  One block per patch.
+__global__ void xwall_kernel(const uint8_t *flags, const Geom g, uint32_t *xwall)
+{
+    const int lp = blockIdx.x;
+    const uint8_t *f = flags + (int64_t)lp * g.fs;
+    const int n1 = g.n[1], n2 = g.n[2];
+    const uint8_t f_lo = f[flag_index(g, -1, 0, 0)], f_hi = f[flag_index(g, g.n[0], 0, 0)];
+    int lo = f_lo != 0 && n1 >= 3 && n2 >= 3, hi = f_hi != 0 && n1 >= 3 && n2 >= 3;
+    for (int k = threadIdx.x; k < n1 * n2; k += blockDim.x) {
+        const int y = k % n1, z = k / n1;
+        lo &= f[flag_index(g, -1, y, z)] == f_lo;
+        hi &= f[flag_index(g, g.n[0], y, z)] == f_hi;
+    }
+    lo = __syncthreads_and(lo);
+    hi = __syncthreads_and(hi);
+    if (threadIdx.x == 0) xwall[lp] = (uint32_t)lo | (uint32_t)hi << 1 | (uint32_t)f_lo << 8 | (uint32_t)f_hi << 16;
+}
+
+cudaError_t launch_xwall(const uint8_t *flags, int nlocal, const Geom &g, uint32_t *xwall, cudaStream_t s)
+{
+    if (nlocal > 0) xwall_kernel<<<nlocal, 256, 0, s>>>(flags, g, xwall);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom &g,
+                              cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>(n, 148 * 64);
-    tile_solid_kernel<<<(unsigned)blocks, SWEEP_BX * SWEEP_BY, 0, s>>>(tiles, n, kind, g);
+    tile_solid_kernel<<<(unsigned)blocks, SWEEP_BX * SWEEP_BY, 0, s>>>(tiles, n, kind, xwall, g);
     return cudaGetLastError();
 }
 

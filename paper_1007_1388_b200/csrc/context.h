@@ -104,8 +104,11 @@ struct lbm_ctx {
     uint32_t *wmask = nullptr;  // wall-neighbour masks of kind-1 cells (flag layout)
     Checker chk;                  // checked build only (kernels.cuh): shadow arrays of the grids
     unsigned long long chk_seq = 0;
-    BbEntry *bb_list = nullptr;  // wall-adjacent fluid cells, patch * fs + e ascending (launch_bb_list)
+    BbEntry *bb_list = nullptr;  // wall-adjacent fluid cells in memory order, per step (launch_bb_list)
     int64_t bb_n = 0;
+    BbEntry *bb_full = nullptr;  // every wall link: the fills after set_pdfs / set_flags (= bb_list's links in AA)
+    int64_t bb_full_n = 0;
+    uint32_t *xwall = nullptr;   // [nlocal] uniform-wall x sides (launch_xwall)
     void *corr = nullptr;
     int *d_origin = nullptr;
     ExSet ex[3];               // indexed by ExKind
@@ -253,8 +256,9 @@ constexpr bool kChecked = true;
 #else
 constexpr bool kChecked = false;
 #endif
-// The bounce-back list kernel on grid gi (mode: aux_kernels.cu bb_list_kernel).
-lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s);
+// The bounce-back list kernel on grid gi (mode: aux_kernels.cu bb_list_kernel);
+// full: every link (after set_pdfs / set_flags), else the per-step list.
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s, bool full = false);
 
 void release_boxes(lbm_ctx *ctx, DevBoxes &b);
 

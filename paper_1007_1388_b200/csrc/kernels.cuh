@@ -31,9 +31,11 @@ constexpr int SWEEP_BY = 4;
 //              addresses live through the collision);
 //   push[i]  : AA PULL scatter target x + e_i in slot i: i * qs + e_i . (1, px, plane);
 //   gpush[i] : e_ix != 0, the x-ghost column target of a row-end scatter:
-//              i * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy.
+//              i * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy;
+//   gwall[i] : e_ix != 0, the half-way bounce-back slot of the x-ghost wall
+//              cell x + e_i: opp(i) * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy.
 struct DirOffsets {
-    int64_t pull[Q], gpull[Q], slot[Q], oslot[Q], push[Q], gpush[Q];
+    int64_t pull[Q], gpull[Q], slot[Q], oslot[Q], push[Q], gpush[Q], gwall[Q];
 };
 void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o);
 
@@ -155,11 +157,22 @@ cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list
 // Building the list (kind == 1 cells of all `total` flag-layout elements): per-chunk
 // counts (bb_list_chunks(total) of them), then, with their exclusive scan, the entries.
 int64_t bb_list_chunks(int64_t total);
-cudaError_t launch_bb_list_count(const uint8_t *kind, int64_t total, int64_t *counts, cudaStream_t s);
-cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags, int64_t total,
-                                 const Geom &g, const int64_t *offsets, BbEntry *list, cudaStream_t s);
-// Bit 31 of each tile descriptor's patch field: the tile holds a non-fluid cell.
-cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const Geom &g, cudaStream_t s);
+// xwall (launch_xwall; null: every link) drops the x links of the inner face cells
+// of uniform-wall x sides from the list: the two-grid sweep stores those itself.
+cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall, int64_t total,
+                                 const Geom &g, int64_t *counts, cudaStream_t s);
+cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
+                                 const uint32_t *xwall, int64_t total, const Geom &g, const int64_t *offsets,
+                                 BbEntry *list, cudaStream_t s);
+// Per local patch, lo | hi << 1 | f_lo << 8 | f_hi << 16: the -x / +x side is a
+// uniform wall -- every ghost cell its inner face cells (y in [1, n1 - 2], z in
+// [1, n2 - 2]) link to carries the one non-fluid flag f.
+cudaError_t launch_xwall(const uint8_t *flags, int nlocal, const Geom &g, uint32_t *xwall, cudaStream_t s);
+// Tile bits: 31 of the patch field, the tile holds a non-fluid cell; 30 / 29, its
+// patch's -x / +x side is a uniform wall (xwall; null: none), whose flag goes to
+// bits 16-23 / 24-31 of the z field.
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom &g,
+                              cudaStream_t s);
 
 // AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL;
 // variant as launch_sweep.

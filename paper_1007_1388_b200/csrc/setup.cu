@@ -254,23 +254,23 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
     return LBM_OK;
 }
 
-lbm_status build_wall_lists(lbm_ctx *ctx)
+// One bounce-back list (launch_bb_list_count / _write): the kind-1 cells, minus the
+// x links of xwall sides when xwall is given.
+static lbm_status build_list(lbm_ctx *ctx, const uint32_t *xwall, BbEntry **list, int64_t *len)
 {
-    // The captured step graphs hold the old list's pointer and length: drop them
-    // (the next multi-step call re-captures).
-    CK(cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < 2; ++i)
-        if (ctx->graph[i]) {
-            cudaGraphExecDestroy(ctx->graph[i]);
-            ctx->graph[i] = nullptr;
-        }
+    if (*list) {
+        cudaFree(*list);
+        ctx->device_bytes -= *len * (int64_t)sizeof(BbEntry);
+        *list = nullptr;
+    }
+    *len = 0;
     const int64_t total = (int64_t)ctx->dec.nlocal * ctx->g.fs;
     const int64_t nch = bb_list_chunks(total);
     int64_t *d_counts = nullptr;
     lbm_status st = dev_alloc(ctx, &d_counts, (size_t)std::max<int64_t>(nch, 1) * sizeof(int64_t));
     if (st) return st;
     std::vector<int64_t> counts((size_t)nch);
-    cudaError_t e = launch_bb_list_count(ctx->kind, total, d_counts, ctx->stream);
+    cudaError_t e = launch_bb_list_count(ctx->kind, ctx->wmask, xwall, total, ctx->g, d_counts, ctx->stream);
     if (e == cudaSuccess && nch > 0)
         e = cudaMemcpyAsync(counts.data(), d_counts, nch * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -280,31 +280,48 @@ lbm_status build_wall_lists(lbm_ctx *ctx)
         c = n;
         n += t;
     }
-    if (ctx->bb_list) {
-        cudaFree(ctx->bb_list);
-        ctx->device_bytes -= ctx->bb_n * (int64_t)sizeof(BbEntry);
-        ctx->bb_list = nullptr;
-    }
-    ctx->bb_n = 0;
-    if (e == cudaSuccess && n > 0) {
-        if ((st = dev_alloc(ctx, &ctx->bb_list, (size_t)n * sizeof(BbEntry)))) {
-            cudaFree(d_counts);
-            ctx->device_bytes -= std::max<int64_t>(nch, 1) * (int64_t)sizeof(int64_t);
-            return st;
-        }
-        ctx->bb_n = n;
+    if (e == cudaSuccess && n > 0 && !(st = dev_alloc(ctx, list, (size_t)n * sizeof(BbEntry)))) {
+        *len = n;
         e = upload(ctx, d_counts, counts.data(), nch * sizeof(int64_t));
         if (e == cudaSuccess)
-            e = launch_bb_list_write(ctx->kind, ctx->wmask, ctx->flags, total, ctx->g, d_counts, ctx->bb_list,
+            e = launch_bb_list_write(ctx->kind, ctx->wmask, ctx->flags, xwall, total, ctx->g, d_counts, *list,
                                      ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     }
-    for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
-        if (e == cudaSuccess) e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ctx->g, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     cudaFree(d_counts);
     ctx->device_bytes -= std::max<int64_t>(nch, 1) * (int64_t)sizeof(int64_t);
+    if (st) return st;
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "build bounce-back list", __FILE__, __LINE__);
+    ctx->launches += 2;
+    return LBM_OK;
+}
+
+lbm_status build_wall_lists(lbm_ctx *ctx)
+{
+    // The captured step graphs hold the old lists' pointers and lengths: drop them
+    // (the next multi-step call re-captures).
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 2; ++i)
+        if (ctx->graph[i]) {
+            cudaGraphExecDestroy(ctx->graph[i]);
+            ctx->graph[i] = nullptr;
+        }
+    // Two grids: patch x sides that are a uniform wall -- the sweep's row-end lanes
+    // store the x links' bounce-back of the face's inner cells, the per-step list
+    // leaves them out; the full list (every link) serves the fills after set_pdfs /
+    // set_flags.  AA: one list for both.
+    const bool ab = ctx->layout != LBM_LAYOUT_AA;
+    lbm_status st;
+    CK(launch_xwall(ctx->flags, ctx->dec.nlocal, ctx->g, ctx->xwall, ctx->stream));
+    if ((st = build_list(ctx, nullptr, &ctx->bb_full, &ctx->bb_full_n))) return st;
+    if (ab && (st = build_list(ctx, ctx->xwall, &ctx->bb_list, &ctx->bb_n))) return st;
+    cudaError_t e = cudaSuccess;
+    for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
+        if (e == cudaSuccess)
+            e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ab ? ctx->xwall : nullptr, ctx->g, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "build wall lists", __FILE__, __LINE__);
-    ctx->launches += 5;
+    ctx->launches += 4;
     return LBM_OK;
 }
 
@@ -518,7 +535,8 @@ void destroy_ctx(lbm_ctx *ctx)
             if (p) cudaFree(p);
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
-                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list
+                    ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list, ctx->bb_full,
+                    ctx->xwall
 #ifdef LBM_CHECKED
                     , ctx->chk.wr, ctx->chk.rd, ctx->chk.err
 #endif
@@ -762,6 +780,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
     }
     if ((st = chk_alloc(ctx, grid_bytes))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->xwall, (size_t)dec.nlocal * sizeof(uint32_t)))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->wmask, flag_bytes * sizeof(uint32_t)))) return bail(st);

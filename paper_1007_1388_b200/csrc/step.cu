@@ -25,6 +25,7 @@ void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o)
         o.oslot[i] = OPPf(i) * g.qs * esize;
         o.push[i] = (i * g.qs + EXf(i) + yz) * esize;
         o.gpush[i] = (i * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
+        o.gwall[i] = (OPPf(i) * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
     }
 }
 
@@ -215,15 +216,18 @@ void fill_bb_offsets(const Geom &g, int mode, int esize, BbOffsets &o)
     }
 }
 
-lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s)
+lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s, bool full)
 {
-    if (ctx->bb_n == 0) return LBM_OK;
+    const bool aa = ctx->layout == LBM_LAYOUT_AA;
+    const BbEntry *list = full || aa ? ctx->bb_full : ctx->bb_list;
+    const int64_t n = full || aa ? ctx->bb_full_n : ctx->bb_n;
+    if (n == 0) return LBM_OK;
     BbOffsets o;
     fill_bb_offsets(ctx->g, mode, ctx->esize, o);
     cudaError_t e = ctx->esize == 8
-                        ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
+                        ? launch_bb_list<double>((double *)ctx->grid[gi], ctx->flags, list, n,
                                                  (const double *)ctx->corr, ctx->g, mode, o, next_checker(ctx), s)
-                        : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, ctx->bb_list, ctx->bb_n,
+                        : launch_bb_list<float>((float *)ctx->grid[gi], ctx->flags, list, n,
                                                 (const float *)ctx->corr, ctx->g, mode, o, next_checker(ctx), s);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "bounce-back list launch", __FILE__, __LINE__);
     ctx->launches += 1;
@@ -240,7 +244,7 @@ lbm_status refresh_state(lbm_ctx *ctx)
     lbm_status st = exchange_seq(ctx, ctx->cur, ctx->stream, nullptr, aa ? EX_AA1 : EX_AB, false);
     if (st) return st;
     if ((st = chk_clear(ctx, ctx->stream))) return st;
-    if ((st = launch_bb(ctx, ctx->cur, aa ? 1 : 0, ctx->stream))) return st;
+    if ((st = launch_bb(ctx, ctx->cur, aa ? 1 : 0, ctx->stream, true))) return st;
     CK(cudaStreamSynchronize(ctx->stream));
     return chk_report(ctx);
 }

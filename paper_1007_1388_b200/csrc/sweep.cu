@@ -77,6 +77,26 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
         }
     }
     if (DIRECT) direct_stores_x2<real>(a, pc.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);
+    // A row end on a uniform-wall x side (launch_xwall): the half-way bounce-back of
+    // its x links, which the per-step list leaves out -- the links of
+    // a face cell all lead into the compact ghost column, so the lane stores them
+    // without any wall lookup.  Inner face cells only (y, z off the face's rim).
+    const bool inner = y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2;
+    if (inner && (pc.xlo || pc.xhi)) {
+        const bool lo = pc.xlo && x0 == 0 && k0 != 2;
+        const bool hi0 = pc.xhi && x0 == g.n[0] - 1 && k0 != 2, hi1 = pc.xhi && x0 + 1 == g.n[0] - 1 && k1 != 2;
+        if (lo | hi0 | hi1) {
+            real *G = ghost_base(g, a.dst + (int64_t)pc.patch * g.ps, y, z);
+#pragma unroll
+            for (int j = 1; j < Q; ++j) {
+                if (EX(j) == 0 || (EX(j) < 0 ? !lo : !(hi0 | hi1))) continue;
+                real v = EX(j) < 0 || hi0 ? p0[j] : p1[j];
+                const int f = EX(j) < 0 ? pc.flo : pc.fhi;  // the side's wall flag: >= 2 moves
+                if (f >= 2) v += __ldg(a.corr + (f - 2) * Q + OPP(j));
+                gst(a.chk, at<real>(G, a.off.gwall[j]), v);
+            }
+        }
+    }
 }
 
 template <typename real, int MINB>

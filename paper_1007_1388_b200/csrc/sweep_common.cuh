@@ -28,7 +28,9 @@ __device__ __forceinline__ int64_t flag_shift(const Geom &g, int i)
 struct PairCoord {
     int patch, x0, y, z, xend;
     bool valid;
-    bool solid;  // the tile holds a non-fluid cell (launch_tile_solid)
+    bool solid;       // the tile holds a non-fluid cell (launch_tile_solid)
+    bool xlo, xhi;    // the patch's -x / +x side is a uniform wall (launch_xwall) ...
+    int flo, fhi;     // ... with this flag
 };
 
 template <typename real>
@@ -36,12 +38,16 @@ __device__ __forceinline__ PairCoord locate_pair(const SweepArgs<real> &a)
 {
     const int4 t = __ldg(a.tiles + blockIdx.x);
     PairCoord c;
-    c.patch = t.x & 0x7fffffff;
+    c.patch = t.x & 0x1fffffff;
     c.solid = t.x < 0;
+    c.xlo = (t.x >> 30) & 1;
+    c.xhi = (t.x >> 29) & 1;
+    c.flo = (t.w >> 16) & 0xff;
+    c.fhi = (int)((unsigned)t.w >> 24);
     c.x0 = (int)((unsigned)t.y >> 16) + 2 * (int)threadIdx.x;
     c.xend = t.y & 0xffff;
     c.y = (int)((unsigned)t.z >> 16) + (int)threadIdx.y;
-    c.z = t.w;
+    c.z = t.w & 0xffff;
     c.valid = c.x0 < c.xend && c.y < (t.z & 0xffff);
     return c;
 }
