@@ -499,36 +499,40 @@ cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list
 // counts per chunk, the host scans the counts, pass 1 writes each chunk's
 // entries at its offset in order.
 constexpr int kBbChunk = 256 * 8;
-// The wall mask of list entry i (0: not an entry): kind-1 cells, minus the x
-// links of the inner face cells of uniform-wall sides, which the two-grid sweep
-// stores itself (xwall_kernel).
-__device__ __forceinline__ uint32_t bb_entry_mask(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall,
-                                                  const Geom &g, int64_t i)
+// The wall mask of list entry i (0: not an entry): kind-1 cells, minus the links
+// of the inner face cells of uniform-wall sides, which the two-grid sweep stores
+// itself (sidewall_kernel).
+__device__ __forceinline__ uint32_t bb_entry_mask(const uint8_t *kind, const uint32_t *wmask,
+                                                  const unsigned long long *sidewall, const Geom &g, int64_t i)
 {
     if (kind[i] != 1) return 0u;
     uint32_t m = wmask[i];
-    if (xwall) {
+    if (sidewall) {
         const int64_t lp = i / g.fs, e = i - lp * g.fs;
-        const int x = (int)(e % g.fpx) - g.fxo;
         const int64_t r = e / g.fpx;
-        const int y = (int)(r % g.py) - 1, z = (int)(r / g.py) - 1;
-        const uint32_t xw = xwall[lp];
-        const bool inner = y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2;
-        if ((xw & 1u) && inner && x == 0) m &= ~kXM;
-        if ((xw & 2u) && inner && x == g.n[0] - 1) m &= ~kXP;
+        const int p[3] = {(int)(e % g.fpx) - g.fxo, (int)(r % g.py) - 1, (int)(r / g.py) - 1};
+        const unsigned long long sw = sidewall[lp];
+        constexpr unsigned lo_bits[3] = {kXM, kYM, kZM}, hi_bits[3] = {kXP, kYP, kZP};
+        for (int a = 0; a < 3; ++a) {
+            const int b = (a + 1) % 3, c = (a + 2) % 3;
+            const bool inner = p[b] >= 1 && p[b] <= g.n[b] - 2 && p[c] >= 1 && p[c] <= g.n[c] - 2;
+            if (!inner) continue;
+            if (((sw >> (2 * a)) & 1ull) && p[a] == 0) m &= ~lo_bits[a];
+            if (((sw >> (2 * a + 1)) & 1ull) && p[a] == g.n[a] - 1) m &= ~hi_bits[a];
+        }
     }
     return m;
 }
 
 __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
-                                     const uint32_t *xwall, int64_t total, const Geom g, int64_t *counts,
+                                     const unsigned long long *sidewall, int64_t total, const Geom g, int64_t *counts,
                                      BbEntry *list)
 {
     __shared__ int warp_tot[8];
     const int64_t base = (int64_t)blockIdx.x * kBbChunk + (int64_t)threadIdx.x * 8;
     int mine = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) mine += (base + k < total && bb_entry_mask(kind, wmask, xwall, g, base + k)) ? 1 : 0;
+    for (int k = 0; k < 8; ++k) mine += (base + k < total && bb_entry_mask(kind, wmask, sidewall, g, base + k)) ? 1 : 0;
     // block-exclusive scan of the per-thread counts (thread order = index order)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int incl = mine;
@@ -551,7 +555,7 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask,
     int64_t pos = counts[blockIdx.x] + before + incl - mine;
     for (int k = 0; k < 8; ++k) {
         const int64_t i = base + k;
-        const uint32_t m = i < total ? bb_entry_mask(kind, wmask, xwall, g, i) : 0u;
+        const uint32_t m = i < total ? bb_entry_mask(kind, wmask, sidewall, g, i) : 0u;
         if (!m) continue;
         BbEntry en;
         const int64_t lp = i / g.fs, e = i - lp * g.fs;
@@ -572,22 +576,22 @@ __global__ void bb_list_build_kernel(const uint8_t *kind, const uint32_t *wmask,
     }
 }
 
-cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall, int64_t total,
-                                 const Geom &g, int64_t *counts, cudaStream_t s)
+cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const unsigned long long *sidewall,
+                                 int64_t total, const Geom &g, int64_t *counts, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
     if (blocks > 0)
-        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, nullptr, xwall, total, g, counts, nullptr);
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, nullptr, sidewall, total, g, counts, nullptr);
     return cudaGetLastError();
 }
 
 cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
-                                 const uint32_t *xwall, int64_t total, const Geom &g, const int64_t *offsets,
-                                 BbEntry *list, cudaStream_t s)
+                                 const unsigned long long *sidewall, int64_t total, const Geom &g,
+                                 const int64_t *offsets, BbEntry *list, cudaStream_t s)
 {
     const int64_t blocks = (total + kBbChunk - 1) / kBbChunk;
     if (blocks > 0)
-        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, flags, xwall, total, g,
+        bb_list_build_kernel<<<(unsigned)blocks, 256, 0, s>>>(kind, wmask, flags, sidewall, total, g,
                                                               (int64_t *)offsets, list);
     return cudaGetLastError();
 }
@@ -596,10 +600,11 @@ int64_t bb_list_chunks(int64_t total) { return (total + kBbChunk - 1) / kBbChunk
 
 // Tile bits (sweep_common.cuh locate_pair): bit 31 of the patch field, the tile
 // holds a non-fluid cell -- only those tiles read the cells' kinds; bits 30 / 29,
-// the patch's -x / +x side is a uniform wall (xwall) -- the two-grid sweep stores
+// the patch's -x / +x side is a uniform wall (sidewall) -- the two-grid sweep stores
 // the x links' bounce-back of that face's inner cells from its row-end lanes --
 // with the wall's flag in bits 16-23 / 24-31 of the z field.  One block per tile.
-__global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom g)
+__global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, const unsigned long long *sidewall,
+                                  const Geom g)
 {
     for (int64_t b = blockIdx.x; b < n; b += gridDim.x) {
         const int4 t = tiles[b];
@@ -610,47 +615,55 @@ __global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, c
         const bool solid = x < xend && y < yend && kind[(int64_t)patch * g.fs + flag_index(g, x, y, z)] == 2;
         const int any = __syncthreads_or(solid);
         if (threadIdx.x == 0) {
-            const uint32_t xw = xwall ? xwall[patch] : 0u;
-            tiles[b].x = patch | (any ? (int)0x80000000u : 0) | (int)((xw & 1u) << 30) | (int)((xw & 2u) << 28);
-            tiles[b].w = z | (int)((xw & 0xffff00u) << 8);
+            const unsigned long long sw = sidewall ? sidewall[patch] : 0ull;
+            tiles[b].x = patch | (any ? (int)0x80000000u : 0) | (int)((sw & 1u) << 30) | (int)((sw & 2u) << 28);
+            tiles[b].w = z | side_flag(sw, 0) << 16 | side_flag(sw, 1) << 24;
         }
         __syncthreads();
     }
 }
 
-// Per local patch, xwall = lo | hi << 1 | f_lo << 8 | f_hi << 16: a side is a
-// uniform wall (lo / hi) when every ghost cell its face's inner cells (y in
-// [1, n1 - 2], z in [1, n2 - 2]) link to -- the column part y in [0, n1 - 1],
-// z in [0, n2 - 1] -- carries one non-fluid flag f.  One block per patch.
-__global__ void xwall_kernel(const uint8_t *flags, const Geom g, uint32_t *xwall)
+// Per local patch and side s = 2 a + (0 low, 1 high): is the ghost layer's part over
+// the face (the other two coordinates in [0, n - 1]) one non-fluid flag?  The inner
+// face cells (those coordinates in [1, n - 2]) link only there.  One block per patch.
+__global__ void sidewall_kernel(const uint8_t *flags, const Geom g, unsigned long long *sidewall)
 {
     const int lp = blockIdx.x;
     const uint8_t *f = flags + (int64_t)lp * g.fs;
-    const int n1 = g.n[1], n2 = g.n[2];
-    const uint8_t f_lo = f[flag_index(g, -1, 0, 0)], f_hi = f[flag_index(g, g.n[0], 0, 0)];
-    int lo = f_lo != 0 && n1 >= 3 && n2 >= 3, hi = f_hi != 0 && n1 >= 3 && n2 >= 3;
-    for (int k = threadIdx.x; k < n1 * n2; k += blockDim.x) {
-        const int y = k % n1, z = k / n1;
-        lo &= f[flag_index(g, -1, y, z)] == f_lo;
-        hi &= f[flag_index(g, g.n[0], y, z)] == f_hi;
+    unsigned long long out = 0;
+    for (int side = 0; side < 6; ++side) {
+        const int a = side / 2, b = (a + 1) % 3, c = (a + 2) % 3;
+        const int na = g.n[a], nb = g.n[b], nc = g.n[c];
+        int p[3];
+        p[a] = side % 2 ? na : -1;
+        p[b] = 0;
+        p[c] = 0;
+        const uint8_t f0 = f[flag_index(g, p[0], p[1], p[2])];
+        int ok = f0 != 0 && nb >= 3 && nc >= 3;
+        for (int k = threadIdx.x; k < nb * nc; k += blockDim.x) {
+            p[b] = k % nb;
+            p[c] = k / nb;
+            ok &= f[flag_index(g, p[0], p[1], p[2])] == f0;
+        }
+        ok = __syncthreads_and(ok);
+        if (ok) out |= 1ull << side | (unsigned long long)f0 << (8 + 8 * side);
     }
-    lo = __syncthreads_and(lo);
-    hi = __syncthreads_and(hi);
-    if (threadIdx.x == 0) xwall[lp] = (uint32_t)lo | (uint32_t)hi << 1 | (uint32_t)f_lo << 8 | (uint32_t)f_hi << 16;
+    if (threadIdx.x == 0) sidewall[lp] = out;
 }
 
-cudaError_t launch_xwall(const uint8_t *flags, int nlocal, const Geom &g, uint32_t *xwall, cudaStream_t s)
+cudaError_t launch_sidewall(const uint8_t *flags, int nlocal, const Geom &g, unsigned long long *sidewall,
+                            cudaStream_t s)
 {
-    if (nlocal > 0) xwall_kernel<<<nlocal, 256, 0, s>>>(flags, g, xwall);
+    if (nlocal > 0) sidewall_kernel<<<nlocal, 256, 0, s>>>(flags, g, sidewall);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom &g,
-                              cudaStream_t s)
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const unsigned long long *sidewall,
+                              const Geom &g, cudaStream_t s)
 {
     if (n <= 0) return cudaSuccess;
     const int64_t blocks = std::min<int64_t>(n, 148 * 64);
-    tile_solid_kernel<<<(unsigned)blocks, SWEEP_BX * SWEEP_BY, 0, s>>>(tiles, n, kind, xwall, g);
+    tile_solid_kernel<<<(unsigned)blocks, SWEEP_BX * SWEEP_BY, 0, s>>>(tiles, n, kind, sidewall, g);
     return cudaGetLastError();
 }
 

@@ -108,7 +108,7 @@ struct lbm_ctx {
     int64_t bb_n = 0;
     BbEntry *bb_full = nullptr;  // every wall link: the fills after set_pdfs / set_flags (= bb_list's links in AA)
     int64_t bb_full_n = 0;
-    uint32_t *xwall = nullptr;   // [nlocal] uniform-wall x sides (launch_xwall)
+    unsigned long long *sidewall = nullptr;  // [nlocal] uniform-wall sides (launch_sidewall)
     void *corr = nullptr;
     int *d_origin = nullptr;
     ExSet ex[3];               // indexed by ExKind

@@ -33,9 +33,11 @@ constexpr int SWEEP_BY = 4;
 //   gpush[i] : e_ix != 0, the x-ghost column target of a row-end scatter:
 //              i * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy;
 //   gwall[i] : e_ix != 0, the half-way bounce-back slot of the x-ghost wall
-//              cell x + e_i: opp(i) * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy.
+//              cell x + e_i: opp(i) * gq + (e_ix < 0 ? 0 : gside) + e_iy + e_iz * gy;
+//   wall[i]  : the same slot of a wall cell x + e_i in the main slices (a y / z
+//              ghost row or plane): opp(i) * qs + e_i . (1, px, plane).
 struct DirOffsets {
-    int64_t pull[Q], gpull[Q], slot[Q], oslot[Q], push[Q], gpush[Q], gwall[Q];
+    int64_t pull[Q], gpull[Q], slot[Q], oslot[Q], push[Q], gpush[Q], gwall[Q], wall[Q];
 };
 void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o);
 
@@ -73,6 +75,7 @@ struct SweepArgs {
     Geom g;
     real omega;
     const int4 *tiles;      // device: one descriptor per block (context.h DevBoxes)
+    const unsigned long long *sidewall = nullptr;  // [patch] uniform-wall sides (launch_sidewall), two grids
     // Direct ghost stores: [nlocal][18][2] base of the neighbour patch (same GPU,
     // or peer-mapped) in grid i, null where the copy path serves it.  Face / edge
     // cells store their outgoing PDFs into that patch's ghost cells of grid dsti.
@@ -157,22 +160,25 @@ cudaError_t launch_bb_list(real *grid, const uint8_t *flags, const BbEntry *list
 // Building the list (kind == 1 cells of all `total` flag-layout elements): per-chunk
 // counts (bb_list_chunks(total) of them), then, with their exclusive scan, the entries.
 int64_t bb_list_chunks(int64_t total);
-// xwall (launch_xwall; null: every link) drops the x links of the inner face cells
-// of uniform-wall x sides from the list: the two-grid sweep stores those itself.
-cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const uint32_t *xwall, int64_t total,
-                                 const Geom &g, int64_t *counts, cudaStream_t s);
+// sidewall (launch_sidewall; null: every link) drops the links of the inner face
+// cells of uniform-wall sides from the list: the two-grid sweep stores those itself.
+cudaError_t launch_bb_list_count(const uint8_t *kind, const uint32_t *wmask, const unsigned long long *sidewall,
+                                 int64_t total, const Geom &g, int64_t *counts, cudaStream_t s);
 cudaError_t launch_bb_list_write(const uint8_t *kind, const uint32_t *wmask, const uint8_t *flags,
-                                 const uint32_t *xwall, int64_t total, const Geom &g, const int64_t *offsets,
-                                 BbEntry *list, cudaStream_t s);
-// Per local patch, lo | hi << 1 | f_lo << 8 | f_hi << 16: the -x / +x side is a
-// uniform wall -- every ghost cell its inner face cells (y in [1, n1 - 2], z in
-// [1, n2 - 2]) link to carries the one non-fluid flag f.
-cudaError_t launch_xwall(const uint8_t *flags, int nlocal, const Geom &g, uint32_t *xwall, cudaStream_t s);
+                                 const unsigned long long *sidewall, int64_t total, const Geom &g,
+                                 const int64_t *offsets, BbEntry *list, cudaStream_t s);
+// Per local patch, bits s = 2 axis + (0 low, 1 high): that side is a uniform wall --
+// every ghost cell the side's inner face cells (the other two coordinates in
+// [1, n - 2]) link to, i.e. the ghost layer's part over the face, carries one
+// non-fluid flag, kept in bits 8 + 8 s .. 15 + 8 s.
+cudaError_t launch_sidewall(const uint8_t *flags, int nlocal, const Geom &g, unsigned long long *sidewall,
+                            cudaStream_t s);
+__host__ __device__ constexpr int side_flag(unsigned long long sw, int side) { return (int)((sw >> (8 + 8 * side)) & 0xff); }
 // Tile bits: 31 of the patch field, the tile holds a non-fluid cell; 30 / 29, its
-// patch's -x / +x side is a uniform wall (xwall; null: none), whose flag goes to
-// bits 16-23 / 24-31 of the z field.
-cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const uint32_t *xwall, const Geom &g,
-                              cudaStream_t s);
+// patch's -x / +x side is a uniform wall (sidewall; null: none), whose flag goes
+// to bits 16-23 / 24-31 of the z field.
+cudaError_t launch_tile_solid(int4 *tiles, int64_t n, const uint8_t *kind, const unsigned long long *sidewall,
+                              const Geom &g, cudaStream_t s);
 
 // AA-pattern in-place sweeps (sweep_aa.cu): pull = true -> PULL kernel, else LOCAL;
 // variant as launch_sweep.

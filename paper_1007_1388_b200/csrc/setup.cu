@@ -255,8 +255,8 @@ lbm_status update_seg_masks(lbm_ctx *ctx, const uint8_t *gflags)
 }
 
 // One bounce-back list (launch_bb_list_count / _write): the kind-1 cells, minus the
-// x links of xwall sides when xwall is given.
-static lbm_status build_list(lbm_ctx *ctx, const uint32_t *xwall, BbEntry **list, int64_t *len)
+// links the two-grid sweep stores itself when sidewall is given.
+static lbm_status build_list(lbm_ctx *ctx, const unsigned long long *sidewall, BbEntry **list, int64_t *len)
 {
     if (*list) {
         cudaFree(*list);
@@ -270,7 +270,7 @@ static lbm_status build_list(lbm_ctx *ctx, const uint32_t *xwall, BbEntry **list
     lbm_status st = dev_alloc(ctx, &d_counts, (size_t)std::max<int64_t>(nch, 1) * sizeof(int64_t));
     if (st) return st;
     std::vector<int64_t> counts((size_t)nch);
-    cudaError_t e = launch_bb_list_count(ctx->kind, ctx->wmask, xwall, total, ctx->g, d_counts, ctx->stream);
+    cudaError_t e = launch_bb_list_count(ctx->kind, ctx->wmask, sidewall, total, ctx->g, d_counts, ctx->stream);
     if (e == cudaSuccess && nch > 0)
         e = cudaMemcpyAsync(counts.data(), d_counts, nch * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -284,7 +284,7 @@ static lbm_status build_list(lbm_ctx *ctx, const uint32_t *xwall, BbEntry **list
         *len = n;
         e = upload(ctx, d_counts, counts.data(), nch * sizeof(int64_t));
         if (e == cudaSuccess)
-            e = launch_bb_list_write(ctx->kind, ctx->wmask, ctx->flags, xwall, total, ctx->g, d_counts, *list,
+            e = launch_bb_list_write(ctx->kind, ctx->wmask, ctx->flags, sidewall, total, ctx->g, d_counts, *list,
                                      ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     }
@@ -306,19 +306,19 @@ lbm_status build_wall_lists(lbm_ctx *ctx)
             cudaGraphExecDestroy(ctx->graph[i]);
             ctx->graph[i] = nullptr;
         }
-    // Two grids: patch x sides that are a uniform wall -- the sweep's row-end lanes
-    // store the x links' bounce-back of the face's inner cells, the per-step list
+    // Two grids: patch sides that are a uniform wall -- the sweep's face lanes store
+    // the bounce-back of the face's inner cells' links through it, the per-step list
     // leaves them out; the full list (every link) serves the fills after set_pdfs /
     // set_flags.  AA: one list for both.
     const bool ab = ctx->layout != LBM_LAYOUT_AA;
     lbm_status st;
-    CK(launch_xwall(ctx->flags, ctx->dec.nlocal, ctx->g, ctx->xwall, ctx->stream));
+    CK(launch_sidewall(ctx->flags, ctx->dec.nlocal, ctx->g, ctx->sidewall, ctx->stream));
     if ((st = build_list(ctx, nullptr, &ctx->bb_full, &ctx->bb_full_n))) return st;
-    if (ab && (st = build_list(ctx, ctx->xwall, &ctx->bb_list, &ctx->bb_n))) return st;
+    if (ab && (st = build_list(ctx, ctx->sidewall, &ctx->bb_list, &ctx->bb_n))) return st;
     cudaError_t e = cudaSuccess;
     for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
         if (e == cudaSuccess)
-            e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ab ? ctx->xwall : nullptr, ctx->g, ctx->stream);
+            e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ab ? ctx->sidewall : nullptr, ctx->g, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "build wall lists", __FILE__, __LINE__);
     ctx->launches += 4;
@@ -536,7 +536,7 @@ void destroy_ctx(lbm_ctx *ctx)
     void *ptrs[] = {ctx->grid[0], ctx->grid[1], ctx->flags, ctx->kind, ctx->wmask, ctx->corr, ctx->d_origin, ctx->sendbuf,
                     ctx->recvbuf,
                     ctx->box_all.desc, ctx->box_shell.desc, ctx->box_interior.desc, ctx->bb_list, ctx->bb_full,
-                    ctx->xwall
+                    ctx->sidewall
 #ifdef LBM_CHECKED
                     , ctx->chk.wr, ctx->chk.rd, ctx->chk.err
 #endif
@@ -780,7 +780,7 @@ lbm_status create_impl(const lbm_config *cfg, lbm_ctx **out)
         if (cudaMemsetAsync(ctx->grid[i], 0, grid_bytes, ctx->stream) != cudaSuccess) return bail(LBM_ERR_CUDA);
     }
     if ((st = chk_alloc(ctx, grid_bytes))) return bail(st);
-    if ((st = dev_alloc(ctx, &ctx->xwall, (size_t)dec.nlocal * sizeof(uint32_t)))) return bail(st);
+    if ((st = dev_alloc(ctx, &ctx->sidewall, (size_t)dec.nlocal * sizeof(unsigned long long)))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->flags, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->kind, flag_bytes))) return bail(st);
     if ((st = dev_alloc(ctx, &ctx->wmask, flag_bytes * sizeof(uint32_t)))) return bail(st);

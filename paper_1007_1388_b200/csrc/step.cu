@@ -26,6 +26,7 @@ void fill_dir_offsets(const Geom &g, bool aa, int esize, DirOffsets &o)
         o.push[i] = (i * g.qs + EXf(i) + yz) * esize;
         o.gpush[i] = (i * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
         o.gwall[i] = (OPPf(i) * g.gq + (EXf(i) < 0 ? 0 : g.gside) + EYf(i) + EZf(i) * (int64_t)g.gy) * esize;
+        o.wall[i] = (OPPf(i) * g.qs + EXf(i) + yz) * esize;
     }
 }
 
@@ -114,6 +115,7 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
     a.g = ctx->g;
     a.omega = (real)ctx->cfg.omega;
     a.tiles = b.desc;
+    a.sidewall = ctx->sidewall;
     a.dnbr = ctx->ldirect ? (real *const *)ctx->d_dnbr : nullptr;
     a.dsti = ctx->layout == LBM_LAYOUT_AA ? 0 : 1 - ctx->cur;
     fill_dir_offsets(ctx->g, ctx->layout == LBM_LAYOUT_AA, (int)sizeof(real), a.off);

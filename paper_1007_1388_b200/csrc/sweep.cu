@@ -23,6 +23,45 @@
 
 namespace lbm {
 
+// The bounce-back through a uniform-wall y (A = 1) or z (A = 2) face of a cell pair
+// on it: c the pair's coordinate along A, o its other inner coordinate (z / y);
+// in0 / in1: the cell is fluid and off the face's x rim.  d: the pair's first
+// cell in the destination grid.
+template <typename real, int A>
+__device__ __forceinline__ void face_wall_stores(const SweepArgs<real> &a, real *d, unsigned long long sw, int c,
+                                                 int o, bool in0, bool in1, const real *p0, const real *p1)
+{
+    using V2 = typename Vec2<real>::T;
+    const Geom &g = a.g;
+    const int B = A == 1 ? 2 : 1;  // the other coordinate's axis
+    if (o < 1 || o > g.n[B] - 2 || !(in0 | in1)) return;
+    const int side = c == 0 ? 2 * A : (c == g.n[A] - 1 ? 2 * A + 1 : -1);
+    if (side < 0 || !((sw >> side) & 1ull)) return;
+    const int s = side & 1 ? 1 : -1;
+    const int f = side_flag(sw, side);
+#pragma unroll
+    for (int j = 1; j < Q; ++j) {
+        if ((A == 1 ? EY(j) : EZ(j)) != 1 && (A == 1 ? EY(j) : EZ(j)) != -1) continue;
+        if ((A == 1 ? EY(j) : EZ(j)) != s) continue;
+        real v0 = p0[j], v1 = p1[j];
+        if (f >= 2) {
+            const real cj = __ldg(a.corr + (f - 2) * Q + OPP(j));
+            v0 += cj;
+            v1 += cj;
+        }
+        real *t = at<real>(d, a.off.wall[j]);
+        if (EX(j) == 0 && in0 && in1) {
+            V2 w;
+            w.x = v0;
+            w.y = v1;
+            gst(a.chk, reinterpret_cast<V2 *>(t), w);
+        } else {
+            if (in0) gst(a.chk, t, v0);
+            if (in1) gst(a.chk, t + 1, v1);
+        }
+    }
+}
+
 // One thread = the cell pair (x0, x0 + 1) of one row; block (32, 4) threads =
 // 64 x 4 cells of one z plane.  The sweep carries no wall logic: the pull is
 // branch-free because the wall slots it reads already hold the half-way
@@ -77,12 +116,13 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
         }
     }
     if (DIRECT) direct_stores_x2<real>(a, pc.patch, x0, y, z, k0 != 2, k1 != 2, p0, p1, nb_x);
-    // A row end on a uniform-wall x side (launch_xwall): the half-way bounce-back of
-    // its x links, which the per-step list leaves out -- the links of
-    // a face cell all lead into the compact ghost column, so the lane stores them
-    // without any wall lookup.  Inner face cells only (y, z off the face's rim).
-    const bool inner = y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2;
-    if (inner && (pc.xlo || pc.xhi)) {
+    // Uniform-wall sides (launch_sidewall): the half-way bounce-back of the
+    // links through such a face, which the per-step list leaves out, stored by the
+    // face cells themselves -- every link of an inner face cell through the face
+    // leads into the ghost layer over it, so no wall lookup is needed.  x: the
+    // row-end lanes, into the compact ghost column; y / z: whole face rows /
+    // planes (warp-uniform), into the ghost rows / planes of the main slices.
+    if (y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2 && (pc.xlo || pc.xhi)) {
         const bool lo = pc.xlo && x0 == 0 && k0 != 2;
         const bool hi0 = pc.xhi && x0 == g.n[0] - 1 && k0 != 2, hi1 = pc.xhi && x0 + 1 == g.n[0] - 1 && k1 != 2;
         if (lo | hi0 | hi1) {
@@ -96,6 +136,12 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
                 gst(a.chk, at<real>(G, a.off.gwall[j]), v);
             }
         }
+    }
+    if (a.sidewall && (y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1)) {
+        const unsigned long long sw = __ldg(a.sidewall + pc.patch);
+        const bool in0 = k0 != 2 && x0 >= 1 && x0 <= g.n[0] - 2, in1 = k1 != 2 && x0 + 1 <= g.n[0] - 2;
+        face_wall_stores<real, 1>(a, d, sw, y, z, in0, in1, p0, p1);
+        face_wall_stores<real, 2>(a, d, sw, z, y, in0, in1, p0, p1);
     }
 }
 

@@ -29,7 +29,7 @@ struct PairCoord {
     int patch, x0, y, z, xend;
     bool valid;
     bool solid;       // the tile holds a non-fluid cell (launch_tile_solid)
-    bool xlo, xhi;    // the patch's -x / +x side is a uniform wall (launch_xwall) ...
+    bool xlo, xhi;    // the patch's -x / +x side is a uniform wall (launch_sidewall) ...
     int flo, fhi;     // ... with this flag
 };
 
