@@ -106,7 +106,7 @@ struct lbm_ctx {
     unsigned long long chk_seq = 0;
     BbEntry *bb_list = nullptr;  // wall-adjacent fluid cells in memory order, per step (launch_bb_list)
     int64_t bb_n = 0;
-    BbEntry *bb_full = nullptr;  // every wall link: the fills after set_pdfs / set_flags (= bb_list's links in AA)
+    BbEntry *bb_full = nullptr;  // every wall link: the fills after set_pdfs / set_flags
     int64_t bb_full_n = 0;
     unsigned long long *sidewall = nullptr;  // [nlocal] uniform-wall sides (launch_sidewall)
     void *corr = nullptr;

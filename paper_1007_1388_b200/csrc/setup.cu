@@ -306,19 +306,17 @@ lbm_status build_wall_lists(lbm_ctx *ctx)
             cudaGraphExecDestroy(ctx->graph[i]);
             ctx->graph[i] = nullptr;
         }
-    // Two grids: patch sides that are a uniform wall -- the sweep's face lanes store
-    // the bounce-back of the face's inner cells' links through it, the per-step list
+    // Patch sides that are a uniform wall: the sweeps' face lanes store the
+    // bounce-back of the face's inner cells' links through it, the per-step list
     // leaves them out; the full list (every link) serves the fills after set_pdfs /
-    // set_flags.  AA: one list for both.
-    const bool ab = ctx->layout != LBM_LAYOUT_AA;
+    // set_flags.
     lbm_status st;
     CK(launch_sidewall(ctx->flags, ctx->dec.nlocal, ctx->g, ctx->sidewall, ctx->stream));
     if ((st = build_list(ctx, nullptr, &ctx->bb_full, &ctx->bb_full_n))) return st;
-    if (ab && (st = build_list(ctx, ctx->sidewall, &ctx->bb_list, &ctx->bb_n))) return st;
+    if ((st = build_list(ctx, ctx->sidewall, &ctx->bb_list, &ctx->bb_n))) return st;
     cudaError_t e = cudaSuccess;
     for (DevBoxes *b : {&ctx->box_all, &ctx->box_shell, &ctx->box_interior})
-        if (e == cudaSuccess)
-            e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ab ? ctx->sidewall : nullptr, ctx->g, ctx->stream);
+        if (e == cudaSuccess) e = launch_tile_solid(b->desc, b->tiles, ctx->kind, ctx->sidewall, ctx->g, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "build wall lists", __FILE__, __LINE__);
     ctx->launches += 4;

@@ -220,9 +220,8 @@ void fill_bb_offsets(const Geom &g, int mode, int esize, BbOffsets &o)
 
 lbm_status launch_bb(lbm_ctx *ctx, int gi, int mode, cudaStream_t s, bool full)
 {
-    const bool aa = ctx->layout == LBM_LAYOUT_AA;
-    const BbEntry *list = full || aa ? ctx->bb_full : ctx->bb_list;
-    const int64_t n = full || aa ? ctx->bb_full_n : ctx->bb_n;
+    const BbEntry *list = full ? ctx->bb_full : ctx->bb_list;
+    const int64_t n = full ? ctx->bb_full_n : ctx->bb_n;
     if (n == 0) return LBM_OK;
     BbOffsets o;
     fill_bb_offsets(ctx->g, mode, ctx->esize, o);

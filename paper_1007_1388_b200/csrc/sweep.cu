@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_x2_kernel(const Swe
     if (DIRECT && (x0 == 0 || x0 + 1 >= g.n[0] - 1)) nb_x = direct_ptr(a, pc.patch, x0 == 0 ? 8 : 9);
     const real *P = a.src + (int64_t)pc.patch * g.ps;
     real p0[Q], p1[Q];
-    pull_pair<real>(a.off, a.chk, P + c, ghost_base(g, P, y, z), x0 == 0, x0 + 1 == g.n[0], x0 + 2 == g.n[0], p0, p1);
+    pull_pair<real>(a.off, a.chk, P + c, ghost_base(g, P, y, z), x0 == 0, x0 + 1 == g.n[0], x0 + 2 == g.n[0], has1,
+                    p0, p1);
     if (k0 == 2 && k1 == 2) return;
     collide_pair(p0, p1, a.omega);
     real *d = a.dst + (int64_t)pc.patch * g.ps + c;

@@ -118,6 +118,64 @@ __device__ __forceinline__ void aa_direct_pair(const SweepArgs<real> &a, int pat
     }
 }
 
+// Uniform-wall patch sides (launch_sidewall; cf. sweep.cu): the half-way
+// bounce-back of the links of a side's inner face cells through it, which the
+// per-step list leaves out, stored by the cells themselves from registers --
+// PULL: out_i + corr into the cell's own slot opp(i) (the list's fix-up, mode 2);
+// LOCAL: out_j + corr into the wall slot j of the ghost cell x + e_j (mode 1).
+// cin0 / cin1: the cell is fluid.
+template <typename real, bool PULL>
+__device__ __forceinline__ void aa_side_wall_stores(const SweepArgs<real> &a, const PairCoord &pc, real *P, real *A,
+                                                    bool cin0, bool cin1, const real *p0, const real *p1)
+{
+    const Geom &g = a.g;
+    const int x0 = pc.x0, y = pc.y, z = pc.z;
+    // x sides: the row-end lanes (side bits and flags in the tile descriptor)
+    if (y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2 && (pc.xlo || pc.xhi)) {
+        const bool lo = pc.xlo && x0 == 0 && cin0;
+        const bool hi0 = pc.xhi && x0 == g.n[0] - 1 && cin0, hi1 = pc.xhi && x0 + 1 == g.n[0] - 1 && cin1;
+        if (lo | hi0 | hi1) {
+            real *G = ghost_base(g, P, y, z);
+#pragma unroll
+            for (int i = 1; i < Q; ++i) {
+                if (EX(i) == 0 || (EX(i) < 0 ? !lo : !(hi0 | hi1))) continue;
+                const bool c1 = EX(i) > 0 && hi1;  // the wall-side cell is the pair's second
+                real v = c1 ? p1[i] : p0[i];
+                const int f = EX(i) < 0 ? pc.flo : pc.fhi;
+                if (f >= 2) v += __ldg(a.corr + (f - 2) * Q + OPP(i));
+                real *t = PULL ? at<real>(A, a.off.oslot[i]) + (c1 ? 1 : 0) : at<real>(G, a.off.gpush[i]);
+                gst(a.chk, t, v);
+            }
+        }
+    }
+    // y / z sides: whole face rows / planes (warp-uniform)
+    if (!(y == 0 || y == g.n[1] - 1 || z == 0 || z == g.n[2] - 1)) return;
+    const unsigned long long sw = __ldg(a.sidewall + pc.patch);
+    const bool xin0 = cin0 && x0 >= 1 && x0 <= g.n[0] - 2, xin1 = cin1 && x0 + 1 <= g.n[0] - 2;
+#pragma unroll
+    for (int A_ = 1; A_ <= 2; ++A_) {
+        const int c = A_ == 1 ? y : z, o = A_ == 1 ? z : y, no = A_ == 1 ? g.n[2] : g.n[1];
+        if (o < 1 || o > no - 2 || !(xin0 | xin1)) continue;
+        const int side = c == 0 ? 2 * A_ : (c == g.n[A_] - 1 ? 2 * A_ + 1 : -1);
+        if (side < 0 || !((sw >> side) & 1ull)) continue;
+        const int s = side & 1 ? 1 : -1;
+        const int f = side_flag(sw, side);
+#pragma unroll
+        for (int i = 1; i < Q; ++i) {
+            if ((A_ == 1 ? EY(i) : EZ(i)) != s) continue;
+            real v0 = p0[i], v1 = p1[i];
+            if (f >= 2) {
+                const real ci = __ldg(a.corr + (f - 2) * Q + OPP(i));
+                v0 += ci;
+                v1 += ci;
+            }
+            real *t = PULL ? at<real>(A, a.off.oslot[i]) : at<real>(A, a.off.push[i]);
+            if (xin0) gst(a.chk, t, v0);
+            if (xin1) gst(a.chk, t + 1, v1);
+        }
+    }
+}
+
 // As the two-grid sweep, the AA kernels carry no wall logic: PULL scatters every
 // out_i to x + e_i, a wall cell included, and the bounce-back list's PULL fix-up
 // (aux_kernels.cu bb_list_kernel, mode 2) then moves out_i + corr from the wall's
@@ -150,7 +208,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
     real p0[Q], p1[Q];
     if (PULL) {
         pull_pair<real>(a.off, a.chk, A, ghost_base(g, (const real *)P, y, z), x0 == 0, x0 + 1 == g.n[0],
-                        x0 + 2 == g.n[0], p0, p1);
+                        x0 + 2 == g.n[0], has1, p0, p1);
     } else {
 #pragma unroll
         for (int i = 0; i < Q; ++i) {
@@ -217,6 +275,7 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
         }
     }
     if (DIRECT) aa_direct_pair<real, PULL>(a, pc.patch, x0, y, z, has1, k0, k1, p0, p1, nb_x);
+    if (a.sidewall) aa_side_wall_stores<real, PULL>(a, pc, P, A, k0 != 2, k1 != 2, p0, p1);
 }
 
 template <typename real>

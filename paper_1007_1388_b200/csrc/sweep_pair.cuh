@@ -21,11 +21,10 @@ namespace lbm {
 // address (with the uniform offset tables 7 % faster in fp64 than two
 // predicated loads, which ptxas issues after the 2-vector loads; 5-6 % faster
 // than a ghost-load branch after the row loads).  All 38 loads are issued
-// before any is consumed.  The phantom partner of an odd row end reads in-bounds
-// garbage that is never used.
+// before any is consumed.
 template <typename real>
 __device__ __forceinline__ void pull_pair(const DirOffsets &o, const Checker &ck, const real *C, const real *G,
-                                          bool lo0, bool hi0, bool hi1, real (&p0)[Q], real (&p1)[Q])
+                                          bool lo0, bool hi0, bool hi1, bool has1, real (&p0)[Q], real (&p1)[Q])
 {
     using V2 = typename Vec2<real>::T;
 #pragma unroll
@@ -37,12 +36,16 @@ __device__ __forceinline__ void pull_pair(const DirOffsets &o, const Checker &ck
             p1[i] = v.y;
         } else {
             const real *gs = at<const real>(G, o.gpull[i]);
+            // the phantom partner of an odd row end (!has1) re-reads the first
+            // cell's value instead of a slot another thread of an in-place (AA)
+            // sweep may be writing
+            const real *s1 = has1 ? s + 1 : s;
             if (EX(i) > 0) {
                 p0[i] = gld(ck, lo0 ? gs : s);
-                p1[i] = gld(ck, s + 1);
+                p1[i] = gld(ck, s1);
             } else {
                 p0[i] = gld(ck, hi0 ? gs : s);
-                p1[i] = gld(ck, hi1 ? gs : s + 1);
+                p1[i] = gld(ck, hi1 ? gs : s1);
             }
         }
     }
