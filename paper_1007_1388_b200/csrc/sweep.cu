@@ -41,8 +41,7 @@ __device__ __forceinline__ void face_wall_stores(const SweepArgs<real> &a, real 
     const int f = side_flag(sw, side);
 #pragma unroll
     for (int j = 1; j < Q; ++j) {
-        if ((A == 1 ? EY(j) : EZ(j)) != 1 && (A == 1 ? EY(j) : EZ(j)) != -1) continue;
-        if ((A == 1 ? EY(j) : EZ(j)) != s) continue;
+        if ((A == 1 ? EY(j) : EZ(j)) != s) continue;  // links through this face only
         real v0 = p0[j], v1 = p1[j];
         if (f >= 2) {
             const real cj = __ldg(a.corr + (f - 2) * Q + OPP(j));
