@@ -20,7 +20,7 @@ KERNELS = {
     "sweep_x2_direct_fp32": "_ZN3lbm15sweep_x2_kernelIfLi5ELb1EEEvNS_9SweepArgsIT_EE",
     "sweep_aa_pull_fp64": "_ZN3lbm18sweep_aa_x2_kernelIdLb1ELi3ELb0EEEvNS_9SweepArgsIT_EE",
     "sweep_aa_local_fp64": "_ZN3lbm18sweep_aa_x2_kernelIdLb0ELi3ELb0EEEvNS_9SweepArgsIT_EE",
-    "bb_list_fp64_mode0": "_ZN3lbm14bb_list_kernelIdLi0EEEvPT_PKhPKNS_7BbEntryElPKS1_NS_4GeomENS_7CheckerE",
+    "bb_list_fp64_mode0": "_ZN3lbm14bb_list_kernelIdLi0EEEvPT_PKhPKNS_7BbEntryElPKS1_NS_4GeomENS_9BbOffsetsENS_7CheckerE",
 }
 
 
