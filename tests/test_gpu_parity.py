@@ -484,3 +484,29 @@ def test_set_flags_again_rebuilds_wall_lists(layout):
         L.close()
     ref = oracle.run(mid, fb, wub, 1.4, 9, nthreads=oracle.max_threads())
     assert max_fluid_diff(got, ref, fb) <= TOL[8]
+
+
+@pytest.mark.parametrize("patch", [(70, 19, 13), (35, 19, 13)])
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_six_moving_walls_vs_oracle(prec, layout, patch):
+    """Every side of the box a moving wall with its own velocity: all six sides are
+    uniform walls, so the sweeps' face cells store the bounce-back through them
+    (with the moving-wall term of their side), while the list handles the rims,
+    edges and corners, where walls of two or three velocities meet; with two
+    patches the sides between them are no walls (direct ghost stores)."""
+    n = (70, 19, 13)
+    fl = np.zeros((n[2] + 2, n[1] + 2, n[0] + 2), np.uint8)
+    # later assignments win on the shared edges / corners
+    fl[:, :, 0] = inputs.VELOCITY0 + 0
+    fl[:, :, -1] = inputs.VELOCITY0 + 1
+    fl[:, 0, :] = inputs.VELOCITY0 + 2
+    fl[:, -1, :] = inputs.VELOCITY0 + 3
+    fl[0, :, :] = inputs.VELOCITY0 + 4
+    fl[-1, :, :] = inputs.VELOCITY0 + 5
+    wu = np.array([[0.0, 0.02, -0.01], [0.0, -0.015, 0.02], [0.03, 0.0, 0.01],
+                   [-0.02, 0.0, -0.025], [0.01, -0.02, 0.0], [0.05, 0.0, 0.0]])
+    f0 = inputs.noise_pdfs(n, seed=53)
+    ref = oracle.run(f0, fl, wu, 1.2, 21, nthreads=oracle.max_threads())
+    got = run_gpu(n, fl, wu, f0, 21, prec, omega=1.2, layout=layout, patch=patch)
+    assert max_fluid_diff(got, ref, fl) <= TOL[prec]
