@@ -625,36 +625,36 @@ __global__ void tile_solid_kernel(int4 *tiles, int64_t n, const uint8_t *kind, c
 
 // Per local patch and side s = 2 a + (0 low, 1 high): is the ghost layer's part over
 // the face (the other two coordinates in [0, n - 1]) one non-fluid flag?  The inner
-// face cells (those coordinates in [1, n - 2]) link only there.  One block per patch.
+// face cells (those coordinates in [1, n - 2]) link only there.  One block per
+// (patch, side); sidewall zeroed before.
 __global__ void sidewall_kernel(const uint8_t *flags, const Geom g, unsigned long long *sidewall)
 {
-    const int lp = blockIdx.x;
+    const int lp = blockIdx.x, side = blockIdx.y;
     const uint8_t *f = flags + (int64_t)lp * g.fs;
-    unsigned long long out = 0;
-    for (int side = 0; side < 6; ++side) {
-        const int a = side / 2, b = (a + 1) % 3, c = (a + 2) % 3;
-        const int na = g.n[a], nb = g.n[b], nc = g.n[c];
-        int p[3];
-        p[a] = side % 2 ? na : -1;
-        p[b] = 0;
-        p[c] = 0;
-        const uint8_t f0 = f[flag_index(g, p[0], p[1], p[2])];
-        int ok = f0 != 0 && nb >= 3 && nc >= 3;
-        for (int k = threadIdx.x; k < nb * nc; k += blockDim.x) {
-            p[b] = k % nb;
-            p[c] = k / nb;
-            ok &= f[flag_index(g, p[0], p[1], p[2])] == f0;
-        }
-        ok = __syncthreads_and(ok);
-        if (ok) out |= 1ull << side | (unsigned long long)f0 << (8 + 8 * side);
+    const int a = side / 2, b = (a + 1) % 3, c = (a + 2) % 3;
+    const int nb = g.n[b], nc = g.n[c];
+    int p[3];
+    p[a] = side % 2 ? g.n[a] : -1;
+    p[b] = 0;
+    p[c] = 0;
+    const uint8_t f0 = f[flag_index(g, p[0], p[1], p[2])];
+    int ok = f0 != 0 && nb >= 3 && nc >= 3;
+    for (int k = threadIdx.x; k < nb * nc && ok; k += blockDim.x) {
+        p[b] = k % nb;
+        p[c] = k / nb;
+        ok &= f[flag_index(g, p[0], p[1], p[2])] == f0;
     }
-    if (threadIdx.x == 0) sidewall[lp] = out;
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0 && ok) atomicOr(sidewall + lp, 1ull << side | (unsigned long long)f0 << (8 + 8 * side));
 }
 
 cudaError_t launch_sidewall(const uint8_t *flags, int nlocal, const Geom &g, unsigned long long *sidewall,
                             cudaStream_t s)
 {
-    if (nlocal > 0) sidewall_kernel<<<nlocal, 256, 0, s>>>(flags, g, sidewall);
+    if (nlocal <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(sidewall, 0, (size_t)nlocal * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    sidewall_kernel<<<dim3((unsigned)nlocal, 6), 256, 0, s>>>(flags, g, sidewall);
     return cudaGetLastError();
 }
 

@@ -241,14 +241,18 @@ __global__ void __launch_bounds__(32 * SWEEP_BY, MINB) sweep_aa_x2_kernel(const 
                     gst(a.chk, t + 1, p1[i]);
                 }
             }
-            if (lo0 || hi1) {
+            // (the inner cells of a uniform-wall x side skip it: aa_side_wall_stores
+            // redirects those links, and the next LOCAL rewrites the wall slot)
+            const bool inner = y >= 1 && y <= g.n[1] - 2 && z >= 1 && z <= g.n[2] - 2;
+            const bool glo = lo0 && !(pc.xlo && inner), ghi = hi1 && !(pc.xhi && inner);
+            if (glo || ghi) {
                 real *G = ghost_base(g, P, y, z);
 #pragma unroll
                 for (int i = 0; i < Q; ++i) {
                     if (EX(i) == 0) continue;
                     real *gt = at<real>(G, a.off.gpush[i]);
-                    if (EX(i) > 0 && hi1) gst(a.chk, gt, p1[i]);
-                    if (EX(i) < 0 && lo0) gst(a.chk, gt, p0[i]);
+                    if (EX(i) > 0 && ghi) gst(a.chk, gt, p1[i]);
+                    if (EX(i) < 0 && glo) gst(a.chk, gt, p0[i]);
                 }
             }
         } else {
