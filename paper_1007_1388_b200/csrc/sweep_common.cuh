@@ -69,7 +69,12 @@ __device__ __forceinline__ real *ghost_base(const Geom &g, real *P, int y, int z
 
 // Global loads / stores of PDF values (kernels.cuh Checker): plain __ldg / store
 // in the product build, checked and recorded in the checked build.
+#ifdef LBM_CHECKED
+// out of line in the checked build: inlined at every access it made ptxas take minutes
+static __device__ __noinline__ void ck_access(const Checker &c, const void *p, int bytes, bool write)
+#else
 __device__ __forceinline__ void ck_access(const Checker &c, const void *p, int bytes, bool write)
+#endif
 {
 #ifdef LBM_CHECKED
     const char *cp = static_cast<const char *>(p);
