@@ -510,3 +510,17 @@ def test_six_moving_walls_vs_oracle(prec, layout, patch):
     ref = oracle.run(f0, fl, wu, 1.2, 21, nthreads=oracle.max_threads())
     got = run_gpu(n, fl, wu, f0, 21, prec, omega=1.2, layout=layout, patch=patch)
     assert max_fluid_diff(got, ref, fl) <= TOL[prec]
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("n", [(40, 2, 5), (40, 5, 2), (1, 8, 9), (2, 3, 3), (66, 3, 4)])
+def test_thin_boxes_vs_oracle(n, layout):
+    """Boxes one to three cells thin along an axis: sides whose faces have no inner
+    cells (uniform-wall detection needs at least 3 cells across the face) leave every
+    link to the bounce-back list; with 3 cells the face has a single inner row."""
+    fl, wu = inputs.ldc_flags(n)
+    f0 = inputs.noise_pdfs(n, seed=61)
+    ref = oracle.run(f0, fl, wu, 1.6, 17)
+    for prec in (8, 4):
+        got = run_gpu(n, fl, wu, f0, 17, prec, omega=1.6, layout=layout)
+        assert max_fluid_diff(got, ref, fl) <= TOL[prec], (n, prec)
