@@ -68,9 +68,7 @@ template <typename real>
 struct SweepArgs {
     const real *src;
     real *dst;
-    const uint8_t *flags;   // [patch][fs] raw cell flags incl. ghost layer (flag layout)
     const uint8_t *kind;    // [patch][fs] 0 fluid (all neighbours fluid), 1 fluid next to a wall, 2 non-fluid
-    const uint32_t *wmask;  // [patch][fs] kind-1 cells: bit j set if x + e_j is non-fluid
     const real *corr;       // [nvel][19]: 6 w_i rho0 (e_i . u_w[k]) rounded to real
     Geom g;
     real omega;

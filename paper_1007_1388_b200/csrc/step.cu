@@ -108,9 +108,7 @@ SweepArgs<real> sweep_args(lbm_ctx *ctx, const DevBoxes &b)
         a.src = (const real *)ctx->grid[ctx->cur];
         a.dst = (real *)ctx->grid[1 - ctx->cur];
     }
-    a.flags = ctx->flags;
     a.kind = ctx->kind;
-    a.wmask = ctx->wmask;
     a.corr = (const real *)ctx->corr;
     a.g = ctx->g;
     a.omega = (real)ctx->cfg.omega;

@@ -11,7 +11,8 @@
 //       out_i + 6 w rho0 e_opp(i).u_w to A[x][opp(i)] (R3).
 // LOCAL (streamed -> swapped): p_i = A[x][i]; collide; A[x][opp(i)] = out_i, and
 //       for walls w = x + e_j the store-side bounce-back A[w][j] = out_j + corr,
-//       which the next PULL gathers branch-free.
+//       which the next PULL gathers branch-free (both bounce-back parts: the
+//       uniform-wall side stores below and the bounce-back list, aux_kernels.cu).
 // Every slot has exactly one writer per step and is read only by it, so both
 // kernels run in place without races; the results equal the two-grid scheme
 // bitwise after every even step count.
