@@ -26,7 +26,7 @@ namespace lbm {
 // The bounce-back through a uniform-wall y (A = 1) or z (A = 2) face of a cell pair
 // on it: c the pair's coordinate along A, o its other inner coordinate (z / y);
 // in0 / in1: the cell is fluid and off the face's x rim.  d: the pair's first
-// cell in the destination grid.
+// cell in the destination grid.  Both sides when the patch is one cell thick.
 template <typename real, int A>
 __device__ __forceinline__ void face_wall_stores(const SweepArgs<real> &a, real *d, unsigned long long sw, int c,
                                                  int o, bool in0, bool in1, const real *p0, const real *p1)
@@ -35,28 +35,31 @@ __device__ __forceinline__ void face_wall_stores(const SweepArgs<real> &a, real 
     const Geom &g = a.g;
     const int B = A == 1 ? 2 : 1;  // the other coordinate's axis
     if (o < 1 || o > g.n[B] - 2 || !(in0 | in1)) return;
-    const int side = c == 0 ? 2 * A : (c == g.n[A] - 1 ? 2 * A + 1 : -1);
-    if (side < 0 || !((sw >> side) & 1ull)) return;
-    const int s = side & 1 ? 1 : -1;
-    const int f = side_flag(sw, side);
 #pragma unroll
-    for (int j = 1; j < Q; ++j) {
-        if ((A == 1 ? EY(j) : EZ(j)) != s) continue;  // links through this face only
-        real v0 = p0[j], v1 = p1[j];
-        if (f >= 2) {
-            const real cj = __ldg(a.corr + (f - 2) * Q + OPP(j));
-            v0 += cj;
-            v1 += cj;
-        }
-        real *t = at<real>(d, a.off.wall[j]);
-        if (EX(j) == 0 && in0 && in1) {
-            V2 w;
-            w.x = v0;
-            w.y = v1;
-            gst(a.chk, reinterpret_cast<V2 *>(t), w);
-        } else {
-            if (in0) gst(a.chk, t, v0);
-            if (in1) gst(a.chk, t + 1, v1);
+    for (int hi = 0; hi < 2; ++hi) {
+        const int side = 2 * A + hi;
+        if (c != (hi ? g.n[A] - 1 : 0) || !((sw >> side) & 1ull)) continue;
+        const int s = hi ? 1 : -1;
+        const int f = side_flag(sw, side);
+#pragma unroll
+        for (int j = 1; j < Q; ++j) {
+            if ((A == 1 ? EY(j) : EZ(j)) != s) continue;  // links through this face only
+            real v0 = p0[j], v1 = p1[j];
+            if (f >= 2) {
+                const real cj = __ldg(a.corr + (f - 2) * Q + OPP(j));
+                v0 += cj;
+                v1 += cj;
+            }
+            real *t = at<real>(d, a.off.wall[j]);
+            if (EX(j) == 0 && in0 && in1) {
+                V2 w;
+                w.x = v0;
+                w.y = v1;
+                gst(a.chk, reinterpret_cast<V2 *>(t), w);
+            } else {
+                if (in0) gst(a.chk, t, v0);
+                if (in1) gst(a.chk, t + 1, v1);
+            }
         }
     }
 }

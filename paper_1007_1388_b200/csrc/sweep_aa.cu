@@ -154,12 +154,12 @@ __device__ __forceinline__ void aa_side_wall_stores(const SweepArgs<real> &a, co
     const unsigned long long sw = __ldg(a.sidewall + pc.patch);
     const bool xin0 = cin0 && x0 >= 1 && x0 <= g.n[0] - 2, xin1 = cin1 && x0 + 1 <= g.n[0] - 2;
 #pragma unroll
-    for (int A_ = 1; A_ <= 2; ++A_) {
+    for (int side = 2; side < 6; ++side) {  // both sides of a one-cell-thick patch
+        const int A_ = side / 2, hi = side & 1;
         const int c = A_ == 1 ? y : z, o = A_ == 1 ? z : y, no = A_ == 1 ? g.n[2] : g.n[1];
         if (o < 1 || o > no - 2 || !(xin0 | xin1)) continue;
-        const int side = c == 0 ? 2 * A_ : (c == g.n[A_] - 1 ? 2 * A_ + 1 : -1);
-        if (side < 0 || !((sw >> side) & 1ull)) continue;
-        const int s = side & 1 ? 1 : -1;
+        if (c != (hi ? g.n[A_] - 1 : 0) || !((sw >> side) & 1ull)) continue;
+        const int s = hi ? 1 : -1;
         const int f = side_flag(sw, side);
 #pragma unroll
         for (int i = 1; i < Q; ++i) {

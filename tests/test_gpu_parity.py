@@ -513,11 +513,12 @@ def test_six_moving_walls_vs_oracle(prec, layout, patch):
 
 
 @pytest.mark.parametrize("layout", [0, 1])
-@pytest.mark.parametrize("n", [(40, 2, 5), (40, 5, 2), (1, 8, 9), (2, 3, 3), (66, 3, 4)])
+@pytest.mark.parametrize("n", [(40, 2, 5), (40, 5, 2), (1, 8, 9), (2, 3, 3), (66, 3, 4), (30, 6, 1), (24, 1, 7)])
 def test_thin_boxes_vs_oracle(n, layout):
     """Boxes one to three cells thin along an axis: sides whose faces have no inner
     cells (uniform-wall detection needs at least 3 cells across the face) leave every
-    link to the bounce-back list; with 3 cells the face has a single inner row."""
+    link to the bounce-back list; with 3 cells the face has a single inner row; one
+    cell thick, a face cell lies on both sides at once (found by the fuzz cases)."""
     fl, wu = inputs.ldc_flags(n)
     f0 = inputs.noise_pdfs(n, seed=61)
     ref = oracle.run(f0, fl, wu, 1.6, 17)
