@@ -195,8 +195,18 @@ def run_reference(args):
                              "sample": sample},
             "e2e": {"value": value, "unit": "MFLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
+
+
+_JSON_OUT = None  # the process's original stdout (see __main__)
+
+
+def emit(line):
+    """The one JSON line -- the only thing this program writes to its stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
@@ -441,7 +451,7 @@ def main():
             "model": {"source": "paper_1007_1388_b200/model.py (P:577-613 re-parameterised: HBM roofline + "
                                 "NVLink 770 GB/s halo)", **est},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     L.close()
     if world > 1:
         dist.barrier()
@@ -478,4 +488,10 @@ def environment() -> dict:
 
 
 if __name__ == "__main__":
+    # Libraries that print to the C stdout (NCCL's version banner at communicator
+    # init) must not precede the JSON line: fd 1 goes to stderr, the line to the
+    # original stdout.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     sys.exit(main())
