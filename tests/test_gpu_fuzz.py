@@ -1,7 +1,8 @@
 """48 seeded random configurations against the oracle: domain and patch sizes (ragged,
 thin, odd), periodic axes, obstacle fractions and kinds, one to three moving-wall
 velocities on random shell sides, both layouts and precisions, graphs on / off,
-step counts odd and even.  Each case exercises a different mix of the sweep's
+step counts odd and even, the three exchange modes (direct stores, NCCL buffers
+with or without overlap, the fused handshake with the rank as its own peer).  Each case exercises a different mix of the sweep's
 uniform-wall side stores, the bounce-back lists, the tiles' non-fluid bits, direct
 ghost stores between patches and periodic self-neighbours."""
 import numpy as np
@@ -40,8 +41,13 @@ def random_case(seed):
     steps = int(rng.integers(1, 12)) * (2 if layout else 1) + int(rng.integers(0, 2))
     graphs = int(rng.integers(0, 2))
     omega = float(rng.uniform(0.6, 1.9))
+    # exchange: direct ghost stores (AUTO), every neighbour through the NCCL path with
+    # the shell / interior overlap (FORCE_BUFFERS), or the fused handshake with the
+    # rank as its own peer (SELF_PEER)
+    exchange = int(rng.choice([0, 0, 1, 2]))
+    overlap = int(rng.integers(0, 2))
     return dict(domain=domain, patch=tuple(patch), periodic=periodic, fl=fl, wu=wu, prec=prec, layout=layout,
-                steps=steps, graphs=graphs, omega=omega)
+                steps=steps, graphs=graphs, omega=omega, exchange=exchange, overlap=overlap)
 
 
 @pytest.mark.parametrize("seed", range(48))
@@ -52,7 +58,7 @@ def test_random_configuration_vs_oracle(seed):
     ref = oracle.run(f0, c["fl"], c["wu"], c["omega"], c["steps"], periodic=c["periodic"],
                      nthreads=oracle.max_threads())
     L = lbm.Lattice(c["domain"], c["patch"], c["omega"], c["prec"], periodic=c["periodic"], layout=c["layout"],
-                    use_graphs=c["graphs"])
+                    use_graphs=c["graphs"], exchange_mode=c["exchange"], overlap=c["overlap"])
     try:
         L.set_flags(c["fl"], c["wu"])
         L.set_pdfs(f0)
@@ -62,4 +68,5 @@ def test_random_configuration_vs_oracle(seed):
         L.close()
     m = c["fl"][1:-1, 1:-1, 1:-1] == 0
     err = float(np.abs(got[m] - ref[m]).max()) if m.any() else 0.0
-    assert err <= TOL[c["prec"]], (c["domain"], c["patch"], c["periodic"], c["prec"], c["layout"], c["steps"], err)
+    assert err <= TOL[c["prec"]], (c["domain"], c["patch"], c["periodic"], c["prec"], c["layout"], c["steps"],
+                                   c["exchange"], err)
