@@ -1,10 +1,11 @@
 """48 seeded random configurations against the oracle: domain and patch sizes (ragged,
 thin, odd), periodic axes, obstacle fractions and kinds, one to three moving-wall
 velocities on random shell sides, both layouts and precisions, graphs on / off,
-step counts odd and even, the three exchange modes (direct stores, NCCL buffers
-with or without overlap, the fused handshake with the rank as its own peer).  Each case exercises a different mix of the sweep's
-uniform-wall side stores, the bounce-back lists, the tiles' non-fluid bits, direct
-ghost stores between patches and periodic self-neighbours."""
+step counts odd and even, and the three exchange modes (direct stores, NCCL buffers
+with or without the overlap, the fused handshake with the rank as its own peer).
+Each case exercises a different mix of the sweep's uniform-wall side stores, the
+bounce-back lists, the tiles' non-fluid bits, direct ghost stores between patches
+and periodic self-neighbours."""
 import numpy as np
 import pytest
 
