@@ -1,4 +1,4 @@
-"""48 seeded random configurations against the oracle: domain and patch sizes (ragged,
+"""96 seeded random configurations against the oracle: domain and patch sizes (ragged,
 thin, odd), periodic axes, obstacle fractions and kinds, one to three moving-wall
 velocities on random shell sides, both layouts and precisions, graphs on / off,
 step counts odd and even, and the three exchange modes (direct stores, NCCL buffers
@@ -51,7 +51,7 @@ def random_case(seed):
                 steps=steps, graphs=graphs, omega=omega, exchange=exchange, overlap=overlap)
 
 
-@pytest.mark.parametrize("seed", range(48))
+@pytest.mark.parametrize("seed", range(96))
 def test_random_configuration_vs_oracle(seed):
     from paper_1007_1388_b200 import lbm
     c = random_case(seed)
